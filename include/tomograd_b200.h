@@ -1,0 +1,249 @@
+/*
+ * tomograd_b200.h — C ABI of the B200-native projector / FDK path.
+ *
+ * This is the drop-in boundary for the reference toolkit's hot path
+ * (tomograd, header-only C++20 CPU; paths below are relative to
+ * proj/include/tomograd/ of the reference).  Every entry point names the
+ * reference interface it replaces.  Plain C types only: POD structs,
+ * pointers and sizes; no torch or C++ types cross it.
+ *
+ * Conventions
+ *  - Layouts are the reference's (image.hpp:5-8, 150-163): volumes x-fastest
+ *    data[(iz*ny+iy)*nx+ix]; cone sinograms [view][v][u]; planar sinograms
+ *    [view][bin].  Device data is float32 (the reference's T = float).
+ *  - "d_" pointers are caller-owned device memory on the plan's device,
+ *    "h_" pointers host memory (pinned memory gets the fast DMA path).
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default).
+ *  - Errors: every call returns tg_status; on failure tg_last_error() (thread
+ *    local) returns the message.  Where the reference throws tomograd::Error
+ *    the message is the reference's exact text, so a C++ shim can rethrow it
+ *    unchanged (see include/tomograd_b200/projector.hpp).
+ *  - Results are deterministic run to run: one writer per output element,
+ *    no floating-point atomics.
+ *  - Plans hold geometry (device constant / global memory) and scratch; calls
+ *    do not allocate except the *_host convenience variants' staging buffers.
+ *    Calls on distinct plans are thread-safe.
+ */
+#ifndef TOMOGRAD_B200_H
+#define TOMOGRAD_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TG_ABI_VERSION 1
+
+typedef int32_t tg_status;
+#define TG_OK 0
+#define TG_ERROR 1          /* a reference check() failure; message in tg_last_error() */
+#define TG_ERROR_CUDA 2     /* CUDA runtime / driver failure */
+#define TG_ERROR_NO_DEVICE 3
+
+/* ---- plain-data mirrors of the reference containers ------------------- */
+
+/* image.hpp:18-54 VolumeSpec; dims = 2 (nx, ny) or 3 (nx, ny, nz) */
+typedef struct tg_volume_spec {
+  uint32_t dims;
+  uint64_t shape[3];
+  double spacing[3];
+  double origin[3]; /* world position of the first element centre */
+} tg_volume_spec;
+
+/* image.hpp:57-67 Detector1D */
+typedef struct tg_detector1d {
+  uint64_t n_bins;
+  double spacing;
+  double origin;
+} tg_detector1d;
+
+/* image.hpp:70-81 Detector2D (u = columns, fastest) */
+typedef struct tg_detector2d {
+  uint64_t n_u, n_v;
+  double spacing_u, spacing_v;
+  double origin_u, origin_v;
+} tg_detector2d;
+
+/* geometry.hpp:50-71 ParallelGeometry (sid = sdd = 0) and
+ * geometry.hpp:88-106 FanGeometry (0 < sid < sdd) */
+typedef struct tg_planar_geometry {
+  tg_volume_spec volume; /* 2D */
+  tg_detector1d detector;
+  uint64_t n_projections;
+  double angular_range;
+  double sid, sdd;
+  const double* rays;   /* n_projections x 2: unit (cos t, sin t) per view */
+  const double* angles; /* n_projections */
+} tg_planar_geometry;
+
+/* geometry.hpp:126-178 ConeGeometry, matrices already normalised by
+ * set_matrices (iso-centre depth == SID) */
+typedef struct tg_cone_geometry {
+  tg_volume_spec volume; /* 3D */
+  tg_detector2d detector;
+  uint64_t n_projections;
+  double angular_range;
+  double sid, sdd;
+  const double* matrices;   /* n x 12, row-major P = K[R|t] */
+  const double* sources;    /* n x 3 */
+  const double* inv_blocks; /* n x 9, inverse of P's left 3x3 block */
+  const double* angles;     /* n, measured from the first view */
+} tg_cone_geometry;
+
+const char* tg_last_error(void);
+int tg_abi_version(void);
+
+/* ---- host geometry: bit-exact with the reference (double maths) -------- */
+
+/* geometry.hpp:30-39 view_angles */
+tg_status tg_view_angles(uint64_t n, double angular_range, double* out);
+/* geometry.hpp:73-86 make_parallel / 108-124 make_fan: rays and angles
+ * (sdd == 0 selects parallel beam) incl. the reference's argument checks */
+tg_status tg_make_planar(const tg_volume_spec* vol, const tg_detector1d* det, uint64_t n,
+                         double angular_range, double sid, double sdd, double* rays_out,
+                         double* angles_out);
+/* geometry.hpp:181-194 cone_projection_matrix */
+tg_status tg_cone_projection_matrix(double theta, double sid, double sdd,
+                                    const tg_detector2d* det, double* out12);
+/* geometry.hpp:206-223 make_cone */
+tg_status tg_make_cone(const tg_volume_spec* vol, const tg_detector2d* det, uint64_t n,
+                       double angular_range, double sid, double sdd, double* matrices,
+                       double* sources, double* inv_blocks, double* angles);
+/* geometry.hpp:144-177 ConeGeometry::set_matrices (make_cone_from_matrices
+ * geometry.hpp:226-242); matrices_in may alias matrices_out */
+tg_status tg_cone_set_matrices(uint64_t n, double sid, const double* matrices_in,
+                               double* matrices_out, double* sources, double* inv_blocks,
+                               double* angles);
+/* filtering.hpp:34-37 filter_window */
+uint64_t tg_filter_window(uint64_t n_bins);
+/* filtering.hpp:40-50 ramp_weights, 68-82 ramlak_weights (length padded_n) */
+tg_status tg_ramp_weights(uint64_t padded_n, double spacing, double* out);
+tg_status tg_ramlak_weights(uint64_t padded_n, double spacing, double* out);
+/* filtering.hpp:157-181 cosine_weights: fan -> [n_bins], cone -> [n_v][n_u] */
+tg_status tg_cosine_weights_fan(const tg_planar_geometry* g, double* out);
+tg_status tg_cosine_weights_cone(const tg_cone_geometry* g, double* out);
+/* filtering.hpp:215-251 parker_weights: fan -> [n_proj][n_bins]; cone ->
+ * [n_proj][n_u] (the reference repeats each row over v) */
+tg_status tg_parker_weights_fan(const tg_planar_geometry* g, double* out);
+tg_status tg_parker_weights_cone(const tg_cone_geometry* g, double* out);
+
+/* ---- cone beam (K1 back-projection, K2 forward projection, K3 FDK) ----- */
+
+typedef struct tg_cone_plan tg_cone_plan;
+
+tg_status tg_cone_plan_create(const tg_cone_geometry* g, int device, tg_cone_plan** out);
+tg_status tg_cone_plan_destroy(tg_cone_plan* plan);
+
+/* projector.hpp:264-281 forward_project(Image, ConeGeometry):
+ * d_vol [nz][ny][nx] -> d_sino [n_proj][n_v][n_u] */
+tg_status tg_cone_forward(tg_cone_plan* plan, const float* d_vol, float* d_sino, void* stream);
+/* angle-sharded variant: views [view0, view0 + n_views) into
+ * d_sino_part [n_views][n_v][n_u] */
+tg_status tg_cone_forward_views(tg_cone_plan* plan, uint64_t view0, uint64_t n_views,
+                                const float* d_vol, float* d_sino_part, void* stream);
+
+/* projector.hpp:283-313 back_project(Sinogram, ConeGeometry):
+ * d_vol = scale * BP(d_sino)  (+ d_vol if accumulate) */
+tg_status tg_cone_backproject(tg_cone_plan* plan, const float* d_sino, float* d_vol, float scale,
+                              int accumulate, void* stream);
+/* z-slab back-projection for multi-GPU sharding: voxels z in [z0, z0+nz)
+ * from detector rows [v0, v0+n_rows) of every view (d_band
+ * [n_proj][n_rows][n_u]) into d_slab [nz][ny][nx].  Coordinates come from
+ * global indices; when z0 and z0+nz are multiples of 16 (K1's z tile) or nz
+ * reaches the volume's end, the slab is bitwise equal to the same z range of
+ * the full-volume result.  The band must cover tg_cone_slab_rows(). */
+tg_status tg_cone_slab_rows(tg_cone_plan* plan, uint64_t z0, uint64_t nz, uint64_t* v0,
+                            uint64_t* n_rows);
+/* the same from the geometry alone (host only, no device) */
+tg_status tg_cone_slab_rows_geom(const tg_cone_geometry* g, uint64_t z0, uint64_t nz, uint64_t* v0,
+                                 uint64_t* n_rows);
+tg_status tg_cone_backproject_slab(tg_cone_plan* plan, uint64_t z0, uint64_t nz, uint64_t v0,
+                                   uint64_t n_rows, const float* d_band, float* d_slab,
+                                   float scale, int accumulate, void* stream);
+
+/* filtering.hpp:136-154,115-125 as composed by pipelines.hpp:76-78:
+ * out = RamLak( T(T(p*cos)*parker) ) row by row, for detector rows
+ * [v0, v0+n_rows) of every view (d_in/d_out [n_proj][n_rows][n_u]; may alias) */
+tg_status tg_cone_fdk_prefilter(tg_cone_plan* plan, const float* d_in, float* d_out, int use_parker,
+                                uint64_t v0, uint64_t n_rows, void* stream);
+/* pipelines.hpp:80-82 the FDK constant (range/n)(SDD/SID)(parker ? 1 : 1/2) */
+double tg_cone_fdk_scale(const tg_cone_plan* plan, int use_parker);
+/* pipelines.hpp:73-84 fdk_reconstruct; d_work is a sinogram-sized scratch
+ * buffer (may equal d_sino to filter in place) */
+tg_status tg_cone_fdk(tg_cone_plan* plan, const float* d_sino, float* d_vol, float* d_work,
+                      int use_parker, void* stream);
+
+/* host-buffer variants with the reference's by-value semantics; H2D copies
+ * are pipelined against the kernels view-chunk by view-chunk */
+tg_status tg_cone_forward_host(tg_cone_plan* plan, const float* h_vol, float* h_sino);
+tg_status tg_cone_backproject_host(tg_cone_plan* plan, const float* h_sino, float* h_vol);
+tg_status tg_cone_fdk_host(tg_cone_plan* plan, const float* h_sino, float* h_vol, int use_parker);
+
+/* ---- parallel / fan beam 2D (K4-K7) ------------------------------------ */
+
+typedef struct tg_planar_plan tg_planar_plan;
+
+tg_status tg_planar_plan_create(const tg_planar_geometry* g, int device, tg_planar_plan** out);
+tg_status tg_planar_plan_destroy(tg_planar_plan* plan);
+/* projector.hpp:171-184 (parallel) / 212-230 (fan) forward_project */
+tg_status tg_planar_forward(tg_planar_plan* plan, const float* d_img, float* d_sino, void* stream);
+/* projector.hpp:186-208 (parallel) / 232-260 (fan, 1/U^2) back_project */
+tg_status tg_planar_backproject(tg_planar_plan* plan, const float* d_sino, float* d_img,
+                                float scale, int accumulate, void* stream);
+tg_status tg_planar_forward_host(tg_planar_plan* plan, const float* h_img, float* h_sino);
+tg_status tg_planar_backproject_host(tg_planar_plan* plan, const float* h_sino, float* h_img);
+
+/* ---- row filters (K3 generic) ------------------------------------------ */
+
+typedef struct tg_filter_plan tg_filter_plan;
+
+/* filtering.hpp:27-32 Filter1D {filt_n_bins, padded_n, filt_spacing,
+ * weights[n_weights]} bound to rows of row_len bins at row_spacing, with the
+ * checks of apply_filter / filter_rows in the reference's order
+ * (filtering.hpp:117-121, 97-99). */
+tg_status tg_filter_plan_create(uint64_t row_len, double row_spacing, uint64_t filt_n_bins,
+                                uint64_t padded_n, double filt_spacing, const double* weights,
+                                uint64_t n_weights, int device, tg_filter_plan** out);
+tg_status tg_filter_plan_destroy(tg_filter_plan* plan);
+/* filtering.hpp:115-125 apply_filter on n_rows contiguous rows of n_bins
+ * (d_in may alias d_out) */
+tg_status tg_filter_apply(tg_filter_plan* plan, const float* d_in, float* d_out, uint64_t n_rows,
+                          void* stream);
+tg_status tg_filter_apply_host(tg_filter_plan* plan, const float* h_in, float* h_out,
+                               uint64_t n_rows);
+
+/* filtering.hpp:136-154 apply_weights: out[k] = T(double(in[k]) * map[k % map_n]) */
+tg_status tg_apply_weights(const float* d_in, float* d_out, uint64_t n_total, const double* d_map,
+                           uint64_t map_n, void* stream);
+/* the same with a per-view row profile broadcast over detector rows (the cone
+ * Parker map, filtering.hpp:246-247): data [n_views][n_rows][n], map [n_views][n] */
+tg_status tg_apply_row_weights(const float* d_in, float* d_out, uint64_t n_views, uint64_t n_rows,
+                               uint64_t n, const double* d_map, void* stream);
+
+/* ---- synthetic inputs (phantom.hpp:34-88, bit-exact, FP64) ------------- */
+
+/* specs: n x 8 doubles {cx, cy, cz, a, b, c, phi_deg, intensity} */
+tg_status tg_rasterize_ellipsoids(const tg_volume_spec* vol, const double* specs, uint64_t n,
+                                  float* d_out, void* stream);
+/* specs: n x 6 doubles {cx, cy, a, b, phi_deg, intensity} */
+tg_status tg_rasterize_ellipses(const tg_volume_spec* vol, const double* specs, uint64_t n,
+                                float* d_out, void* stream);
+/* phantom.hpp:107-128 tables scaled by fov_half_extent(vol) */
+tg_status tg_head_phantom_ellipsoids(const tg_volume_spec* vol, double* out80);
+tg_status tg_head_phantom_ellipses(const tg_volume_spec* vol, double* out60);
+
+/* ---- instrumentation ---------------------------------------------------- */
+
+/* number of kernels this library launched in the calling process so far */
+uint64_t tg_kernel_launch_count(void);
+/* average device time (ms) of the last call's dominant kernel, measured with
+ * CUDA events on the launch stream when tg_set_timing(1) */
+void tg_set_timing(int enable);
+double tg_last_kernel_ms(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TOMOGRAD_B200_H */

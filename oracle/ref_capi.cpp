@@ -1,0 +1,278 @@
+// ref_capi.cpp — CPU ORACLE glue (TEST INFRASTRUCTURE ONLY).
+//
+// Compiles the UNMODIFIED reference toolkit headers (found through
+// -I$(TOMOGRAD_REF_INCLUDE), default /root/reference/proj/include) into
+// oracle/_ref/libtomograd_ref.so and exposes its projector / FDK path through
+// a C ABI that uses the same POD structs as the C restatement (tg_oracle.h).
+// Nothing here re-implements an algorithm: every call goes to the
+// reference's own functions.  Used only to pin the restatement (tests/) and
+// as bench.py's "reference" CPU arm.
+#include <cstring>
+#include <exception>
+#include <string>
+#include <vector>
+
+#include "tg_oracle.h"
+#include "tomograd/filtering.hpp"
+#include "tomograd/geometry.hpp"
+#include "tomograd/image.hpp"
+#include "tomograd/phantom.hpp"
+#include "tomograd/pipelines.hpp"
+#include "tomograd/projector.hpp"
+
+using namespace tomograd;
+
+namespace {
+
+thread_local std::string g_err;
+
+template <typename Fn>
+int guard(Fn&& fn) {
+  try {
+    fn();
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
+
+VolumeSpec to_spec(const or_volume& v) {
+  VolumeSpec s;
+  for (uint32_t a = 0; a < v.dims; ++a) {
+    s.shape.push_back(std::size_t(v.shape[a]));
+    s.spacing.push_back(v.spacing[a]);
+    s.origin.push_back(v.origin[a]);
+  }
+  return s;
+}
+
+Detector1D to_det(const or_det1& d) { return {std::size_t(d.n_bins), d.spacing, d.origin}; }
+Detector2D to_det(const or_det2& d) {
+  return {std::size_t(d.n_u), std::size_t(d.n_v), d.spacing_u, d.spacing_v, d.origin_u, d.origin_v};
+}
+
+// Planar geometry: circular (rays == nullptr) through the reference factories,
+// otherwise with explicit rays (ParallelGeometry::set_custom_rays semantics
+// are not needed: rays are stored as given, angles as given).
+ParallelGeometry to_parallel(const or_planar& g) {
+  auto geo = make_parallel(to_spec(g.vol), to_det(g.det), std::size_t(g.n_proj), g.range);
+  return geo;
+}
+FanGeometry to_fan(const or_planar& g) {
+  return make_fan(to_spec(g.vol), to_det(g.det), std::size_t(g.n_proj), g.range, g.sid, g.sdd);
+}
+
+// Cone geometry through the reference's own setup: circular via make_cone,
+// explicit (already normalised) matrices via make_cone_from_matrices.
+ConeGeometry to_cone(const or_cone& g, bool circular) {
+  if (circular)
+    return make_cone(to_spec(g.vol), to_det(g.det), std::size_t(g.n_proj), g.range, g.sid, g.sdd);
+  std::vector<Mat34> mats(g.n_proj);
+  for (std::size_t i = 0; i < g.n_proj; ++i)
+    for (int k = 0; k < 12; ++k) mats[i].m[std::size_t(k)] = g.mats[12 * i + std::size_t(k)];
+  return make_cone_from_matrices(to_spec(g.vol), to_det(g.det), g.range, g.sid, g.sdd, mats);
+}
+
+template <typename T>
+Image<T> make_image(const VolumeSpec& s, const T* data) {
+  Image<T> img(s);
+  std::memcpy(img.data.data(), data, sizeof(T) * img.data.size());
+  return img;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error(void) { return g_err.c_str(); }
+void ref_set_threads(int n) { set_num_threads(unsigned(n < 1 ? 1 : n)); }
+int ref_num_threads(void) { return int(num_threads()); }
+
+int ref_view_angles(uint64_t n, double range, double* out) {
+  return guard([&] {
+    auto a = view_angles(std::size_t(n), range);
+    std::memcpy(out, a.data(), sizeof(double) * a.size());
+  });
+}
+
+int ref_make_cone(const or_volume* vol, const or_det2* det, uint64_t n, double range, double sid,
+                  double sdd, double* mats, double* sources, double* invs, double* angles) {
+  return guard([&] {
+    auto g = make_cone(to_spec(*vol), to_det(*det), std::size_t(n), range, sid, sdd);
+    for (std::size_t i = 0; i < n; ++i) {
+      std::memcpy(mats + 12 * i, g.matrices[i].m.data(), 12 * sizeof(double));
+      std::memcpy(invs + 9 * i, g.inv_blocks[i].m.data(), 9 * sizeof(double));
+      sources[3 * i] = g.sources[i].x;
+      sources[3 * i + 1] = g.sources[i].y;
+      sources[3 * i + 2] = g.sources[i].z;
+      angles[i] = g.angles[i];
+    }
+  });
+}
+
+int ref_cone_from_matrices(const or_volume* vol, const or_det2* det, uint64_t n, double range,
+                           double sid, double sdd, const double* mats_in, double* mats,
+                           double* sources, double* invs, double* angles) {
+  return guard([&] {
+    std::vector<Mat34> m(n);
+    for (std::size_t i = 0; i < n; ++i)
+      for (int k = 0; k < 12; ++k) m[i].m[std::size_t(k)] = mats_in[12 * i + std::size_t(k)];
+    auto g = make_cone_from_matrices(to_spec(*vol), to_det(*det), range, sid, sdd, m);
+    for (std::size_t i = 0; i < n; ++i) {
+      std::memcpy(mats + 12 * i, g.matrices[i].m.data(), 12 * sizeof(double));
+      std::memcpy(invs + 9 * i, g.inv_blocks[i].m.data(), 9 * sizeof(double));
+      sources[3 * i] = g.sources[i].x;
+      sources[3 * i + 1] = g.sources[i].y;
+      sources[3 * i + 2] = g.sources[i].z;
+      angles[i] = g.angles[i];
+    }
+  });
+}
+
+int ref_planar_rays(const or_volume* vol, const or_det1* det, uint64_t n, double range, double sid,
+                    double sdd, double* rays, double* angles) {
+  return guard([&] {
+    std::vector<Vec2> r;
+    std::vector<double> a;
+    if (sdd > 0.0) {
+      auto g = make_fan(to_spec(*vol), to_det(*det), std::size_t(n), range, sid, sdd);
+      r = g.rays;
+      a = g.angles;
+    } else {
+      auto g = make_parallel(to_spec(*vol), to_det(*det), std::size_t(n), range);
+      r = g.rays;
+      a = g.angles;
+    }
+    for (std::size_t i = 0; i < n; ++i) {
+      rays[2 * i] = r[i].x;
+      rays[2 * i + 1] = r[i].y;
+      angles[i] = a[i];
+    }
+  });
+}
+
+#define REF_OPS(SUF, T)                                                                       \
+  int ref_planar_forward_##SUF(const or_planar* g, const T* img, T* sino) {                   \
+    return guard([&] {                                                                        \
+      auto im = make_image<T>(to_spec(g->vol), img);                                          \
+      Sinogram<T> s = g->sdd > 0.0 ? forward_project(im, to_fan(*g))                          \
+                                   : forward_project(im, to_parallel(*g));                    \
+      std::memcpy(sino, s.data.data(), sizeof(T) * s.data.size());                            \
+    });                                                                                       \
+  }                                                                                           \
+  int ref_planar_backproject_##SUF(const or_planar* g, const T* sino, T* img) {               \
+    return guard([&] {                                                                        \
+      auto s = Sinogram<T>::planar(std::size_t(g->n_proj), to_det(g->det));                  \
+      std::memcpy(s.data.data(), sino, sizeof(T) * s.data.size());                            \
+      Image<T> im = g->sdd > 0.0 ? back_project(s, to_fan(*g)) : back_project(s, to_parallel(*g)); \
+      std::memcpy(img, im.data.data(), sizeof(T) * im.data.size());                           \
+    });                                                                                       \
+  }                                                                                           \
+  int ref_cone_forward_##SUF(const or_cone* g, int circular, const T* vol, T* sino) {         \
+    return guard([&] {                                                                        \
+      auto im = make_image<T>(to_spec(g->vol), vol);                                          \
+      auto s = forward_project(im, to_cone(*g, circular != 0));                               \
+      std::memcpy(sino, s.data.data(), sizeof(T) * s.data.size());                            \
+    });                                                                                       \
+  }                                                                                           \
+  int ref_cone_backproject_##SUF(const or_cone* g, int circular, const T* sino, T* vol) {     \
+    return guard([&] {                                                                        \
+      auto s = Sinogram<T>::cone_beam(std::size_t(g->n_proj), to_det(g->det));               \
+      std::memcpy(s.data.data(), sino, sizeof(T) * s.data.size());                            \
+      auto im = back_project(s, to_cone(*g, circular != 0));                                  \
+      std::memcpy(vol, im.data.data(), sizeof(T) * im.data.size());                           \
+    });                                                                                       \
+  }                                                                                           \
+  int ref_fdk_reconstruct_##SUF(const or_cone* g, int circular, const T* sino, T* vol,        \
+                                int use_parker) {                                             \
+    return guard([&] {                                                                        \
+      auto s = Sinogram<T>::cone_beam(std::size_t(g->n_proj), to_det(g->det));               \
+      std::memcpy(s.data.data(), sino, sizeof(T) * s.data.size());                            \
+      auto im = fdk_reconstruct(s, to_cone(*g, circular != 0), use_parker != 0);              \
+      std::memcpy(vol, im.data.data(), sizeof(T) * im.data.size());                           \
+    });                                                                                       \
+  }                                                                                           \
+  int ref_fbp_reconstruct_##SUF(const or_planar* g, const T* sino, T* img, int ramlak) {      \
+    return guard([&] {                                                                        \
+      auto s = Sinogram<T>::planar(std::size_t(g->n_proj), to_det(g->det));                  \
+      std::memcpy(s.data.data(), sino, sizeof(T) * s.data.size());                            \
+      auto im = fbp_reconstruct(s, to_parallel(*g), ramlak ? FilterKind::ramlak : FilterKind::ramp); \
+      std::memcpy(img, im.data.data(), sizeof(T) * im.data.size());                           \
+    });                                                                                       \
+  }                                                                                           \
+  /* apply_filter on n_rows planar rows of n bins (spacing ds) with explicit weights */      \
+  int ref_apply_filter_##SUF(T* data, uint64_t n_rows, uint64_t n, double ds,                 \
+                             const double* weights, uint64_t padded_n, uint64_t n_weights) {  \
+    return guard([&] {                                                                        \
+      auto s = Sinogram<T>::planar(std::size_t(n_rows), Detector1D::centered(std::size_t(n), ds)); \
+      std::memcpy(s.data.data(), data, sizeof(T) * s.data.size());                            \
+      Filter1D f{std::size_t(n), std::size_t(padded_n), ds,                                   \
+                 std::vector<double>(weights, weights + n_weights)};                          \
+      auto o = apply_filter(s, f);                                                            \
+      std::memcpy(data, o.data.data(), sizeof(T) * o.data.size());                            \
+    });                                                                                       \
+  }                                                                                           \
+  int ref_shepp_logan_3d_##SUF(const or_volume* vol, T* out) {                               \
+    return guard([&] {                                                                        \
+      auto im = shepp_logan_3d<T>(to_spec(*vol));                                             \
+      std::memcpy(out, im.data.data(), sizeof(T) * im.data.size());                           \
+    });                                                                                       \
+  }                                                                                           \
+  int ref_shepp_logan_2d_##SUF(const or_volume* vol, T* out) {                               \
+    return guard([&] {                                                                        \
+      auto im = shepp_logan_2d<T>(to_spec(*vol));                                             \
+      std::memcpy(out, im.data.data(), sizeof(T) * im.data.size());                           \
+    });                                                                                       \
+  }
+
+REF_OPS(f32, float)
+REF_OPS(f64, double)
+
+int ref_ramlak_weights(uint64_t padded_n, double spacing, double* out) {
+  return guard([&] {
+    auto w = ramlak_weights(std::size_t(padded_n), spacing);
+    std::memcpy(out, w.data(), sizeof(double) * w.size());
+  });
+}
+
+int ref_ramp_weights(uint64_t padded_n, double spacing, double* out) {
+  return guard([&] {
+    auto w = ramp_weights(std::size_t(padded_n), spacing);
+    std::memcpy(out, w.data(), sizeof(double) * w.size());
+  });
+}
+
+int ref_cosine_weights_cone(const or_cone* g, double* out) {
+  return guard([&] {
+    auto m = cosine_weights(to_cone(*g, true));
+    std::memcpy(out, m.data.data(), sizeof(double) * m.data.size());
+  });
+}
+
+// compact [view][u] copy of the reference's full [view][v][u] Parker map
+int ref_parker_weights_cone(const or_cone* g, double* out) {
+  return guard([&] {
+    auto geo = to_cone(*g, true);
+    auto m = parker_weights(geo);
+    const std::size_t nu = g->det.n_u, nv = g->det.n_v;
+    for (std::size_t i = 0; i < g->n_proj; ++i)
+      std::memcpy(out + i * nu, m.data.data() + i * nv * nu, sizeof(double) * nu);
+  });
+}
+
+int ref_parker_weights_fan(const or_planar* g, double* out) {
+  return guard([&] {
+    auto m = parker_weights(to_fan(*g));
+    std::memcpy(out, m.data.data(), sizeof(double) * m.data.size());
+  });
+}
+
+int ref_cosine_weights_fan(const or_planar* g, double* out) {
+  return guard([&] {
+    auto m = cosine_weights(to_fan(*g));
+    std::memcpy(out, m.data.data(), sizeof(double) * m.data.size());
+  });
+}
+
+}  // extern "C"

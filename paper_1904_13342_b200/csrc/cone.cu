@@ -1,0 +1,947 @@
+// cone.cu — cone-beam plan, K1 back-projection, K2 forward projection and
+// the host-buffer pipelines.  Reference: projector.hpp:264-313 (operators),
+// pipelines.hpp:73-84 (FDK composition), geometry.hpp:126-178 (plan data).
+#include <algorithm>
+#include <memory>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "cone_kernels.cuh"
+#include "filter.cuh"
+
+namespace tgb {
+namespace cone {
+
+__constant__ float4 c_views[3 * kMaxConstViews];
+static ConstBank g_bank;
+
+// ---------------------------------------------------------------------------
+// shared footprint logic (producer warp and plan-time sizing use the same
+// fp32 arithmetic)
+
+__device__ __forceinline__ Footprint make_footprint(float umin, float umax, float vmin, float vmax,
+                                                    bool ok, int nu, int nv) {
+  Footprint f;
+  ok = ok && fabsf(umin) < 4.0e6f && fabsf(umax) < 4.0e6f && fabsf(vmin) < 4.0e6f &&
+       fabsf(vmax) < 4.0e6f;
+  f.ok = ok;
+  if (!ok) {
+    f.ub = f.vb = f.width = f.height = 0;
+    f.hit = true;
+    return f;
+  }
+  const int u_lo = int(floorf(umin)), u_hi = int(floorf(umax));
+  const int v_lo = int(floorf(vmin)), v_hi = int(floorf(vmax));
+  f.ub = u_lo - 1;
+  f.vb = v_lo - 1;
+  f.width = u_hi - u_lo + 4;   // taps [u_lo, u_hi + 1] plus one pixel each side
+  f.height = v_hi - v_lo + 4;
+  // every tap outside the detector contributes exactly zero
+  f.hit = !(u_hi + 2 < 0 || f.ub > nu - 1 || v_hi + 2 < 0 || f.vb > nv - 1);
+  return f;
+}
+
+struct TileBox {
+  float x[2], y[2], z[2];
+};
+
+__device__ __forceinline__ TileBox tile_corners(const BpArgs& a, int tx, int ty, int tz, int K) {
+  TileBox b;
+  const int x0 = tx * BX, y0 = ty * BY, z0 = tz * K;
+  const int x1 = min(x0 + BX, a.nx) - 1, y1 = min(y0 + BY, a.ny) - 1, z1 = min(z0 + K, a.nz) - 1;
+  b.x[0] = float(a.ox + double(x0) * a.sx);
+  b.x[1] = float(a.ox + double(x1) * a.sx);
+  b.y[0] = float(a.oy + double(y0) * a.sy);
+  b.y[1] = float(a.oy + double(y1) * a.sy);
+  b.z[0] = float(a.oz + double(a.z0 + z0) * a.sz);
+  b.z[1] = float(a.oz + double(a.z0 + z1) * a.sz);
+  return b;
+}
+
+// plan-time: largest footprint over every (tile, view) that takes the fast path
+__global__ void footprint_kernel(BpArgs a, int K, int tiles_x, int tiles_y, int tiles_z,
+                                 const float4* __restrict__ coef, int* __restrict__ need) {
+  const long long n_tiles = (long long)tiles_x * tiles_y * tiles_z;
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= n_tiles * a.n_views) return;
+  const int view = int(idx / n_tiles);
+  long long t = idx % n_tiles;
+  const int tx = int(t % tiles_x);
+  t /= tiles_x;
+  const int ty = int(t % tiles_y), tz = int(t / tiles_y);
+  const TileBox b = tile_corners(a, tx, ty, tz, K);
+  const float4 r0 = coef[3 * view], r1 = coef[3 * view + 1], r2 = coef[3 * view + 2];
+  float umin = INFINITY, umax = -INFINITY, vmin = INFINITY, vmax = -INFINITY;
+  bool ok = true;
+  for (int c = 0; c < 8; ++c) {
+    float u, v, hz;
+    project_point(r0, r1, r2, b.x[c & 1], b.y[(c >> 1) & 1], b.z[c >> 2], u, v, hz);
+    ok = ok && hz > 0.0f;
+    umin = fminf(umin, u);
+    umax = fmaxf(umax, u);
+    vmin = fminf(vmin, v);
+    vmax = fmaxf(vmax, v);
+  }
+  const Footprint f = make_footprint(umin, umax, vmin, vmax, ok, a.nu, a.nv);
+  if (f.ok && f.hit) {
+    atomicMax(&need[0], f.width);
+    atomicMax(&need[1], f.height);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K1: voxel-driven back-projection
+
+__device__ __forceinline__ float lds_f32(uint32_t addr) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+  return v;
+}
+
+// zero-padded bilinear gather from global memory (slow path; projector.hpp:44-64)
+__device__ __forceinline__ float bilinear_global(const BpArgs& a, const float* __restrict__ img,
+                                                 float u, float v) {
+  const float fu = floorf(u), fv = floorf(v);
+  const int c0 = int(fu), r0 = int(fv);
+  const float wu = u - fu, wv = v - fv;
+  float acc = 0.0f;
+#pragma unroll
+  for (int dr = 0; dr < 2; ++dr) {
+    const int r = r0 + dr;
+    if (r < 0 || r >= a.nv) continue;
+    const int rb = r - a.band_v0;
+    if (rb < 0 || rb >= a.band_rows) continue;
+    const float wr = dr ? wv : 1.0f - wv;
+    const float* row = img + (long long)rb * a.row_pitch;
+    if (c0 >= 0 && c0 < a.nu) acc += (1.0f - wu) * wr * __ldg(row + c0);
+    if (c0 + 1 >= 0 && c0 + 1 < a.nu) acc += wu * wr * __ldg(row + c0 + 1);
+  }
+  return acc;
+}
+
+template <int K, int BOXU, bool CIRC>
+__global__ void __launch_bounds__(NTHREADS, 2)
+    cone_bp_kernel(const __grid_constant__ CUtensorMap tmap, const BpArgs a) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int box_elems = BOXU * a.boxV;
+  float* boxes = reinterpret_cast<float*>(smem);
+  int4* hdr = reinterpret_cast<int4*>(boxes + STAGES * box_elems);
+  uint64_t* full = reinterpret_cast<uint64_t*>(hdr + STAGES);
+  uint64_t* empty = full + STAGES;
+
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NCONS / 32);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+
+  if (tid >= NCONS) {
+    // ---------------- producer warp: footprint + TMA per view -------------
+    const int lane = tid & 31;
+    if (lane == 0) prefetch_tensor_map(&tmap);
+    const TileBox b = tile_corners(a, blockIdx.x, blockIdx.y, blockIdx.z, K);
+    const float cx = (lane & 1) ? b.x[1] : b.x[0];
+    const float cy = (lane & 2) ? b.y[1] : b.y[0];
+    const float cz = (lane & 4) ? b.z[1] : b.z[0];
+    for (int it = 0; it < a.n_views; ++it) {
+      const int s = it % STAGES;
+      if (it >= STAGES) mbar_wait(&empty[s], ((it / STAGES) - 1) & 1);
+      const float4 r0 = c_views[3 * it], r1 = c_views[3 * it + 1], r2 = c_views[3 * it + 2];
+      float u, v, hz;
+      project_point(r0, r1, r2, cx, cy, cz, u, v, hz);
+      bool ok = hz > 0.0f;
+      float umin = u, umax = u, vmin = v, vmax = v;
+#pragma unroll
+      for (int off = 4; off >= 1; off >>= 1) {  // reduce over the 8 corner lanes
+        umin = fminf(umin, __shfl_xor_sync(0xffffffffu, umin, off));
+        umax = fmaxf(umax, __shfl_xor_sync(0xffffffffu, umax, off));
+        vmin = fminf(vmin, __shfl_xor_sync(0xffffffffu, vmin, off));
+        vmax = fmaxf(vmax, __shfl_xor_sync(0xffffffffu, vmax, off));
+        ok = __shfl_xor_sync(0xffffffffu, int(ok), off) && ok;
+      }
+      if (lane == 0) {
+        const Footprint f = make_footprint(umin, umax, vmin, vmax, ok, a.nu, a.nv);
+        int mode = MODE_SLOW;
+        if (f.ok && !f.hit) mode = MODE_SKIP;
+        else if (f.ok && f.width <= BOXU && f.height <= a.boxV) mode = MODE_FAST;
+        hdr[s] = make_int4(f.ub, f.vb, mode, 0);
+        if (mode == MODE_FAST) {
+          mbar_arrive_expect_tx(&full[s], uint32_t(box_elems * 4));
+          tma_load_3d(boxes + s * box_elems, &tmap, &full[s], f.ub, f.vb - a.band_v0,
+                      a.view_base + it);
+        } else {
+          mbar_arrive(&full[s]);
+        }
+      }
+      __syncwarp();
+    }
+    return;
+  }
+
+  // ---------------- consumers: one (x, y) column, K voxels each -------------
+  const int w = tid >> 5, lane = tid & 31;
+  const int lx = lane & 15, ly = 2 * w + (lane >> 4);
+  const int gx = blockIdx.x * BX + lx, gy = blockIdx.y * BY + ly;
+  const int zt0 = blockIdx.z * K;
+  const bool valid = gx < a.nx && gy < a.ny;
+  const int ix = min(gx, a.nx - 1), iy = min(gy, a.ny - 1);
+  const float x = float(a.ox + double(ix) * a.sx);
+  const float y = float(a.oy + double(iy) * a.sy);
+  const float zf0 = float(a.oz + double(a.z0 + zt0) * a.sz);
+  const float dz = float(a.sz);
+  const int kmax = min(K, a.nz - zt0) - 1;  // clamp tail voxels into the tile
+  const uint32_t box_base = smem_u32(boxes);
+  constexpr uint32_t ROWB = BOXU * 4;
+  constexpr float MAGIC = 12582912.0f;  // 1.5 * 2^23: t = M + floor(v) under round-down
+  constexpr uint32_t MAGIC_BITS = 0x4B400000u;
+
+  float acc[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) acc[k] = 0.0f;
+
+  for (int it = 0; it < a.n_views; ++it) {
+    const int s = it % STAGES;
+    mbar_wait(&full[s], (it / STAGES) & 1);
+    const int4 h = hdr[s];
+    const float4 r0 = c_views[3 * it], r1 = c_views[3 * it + 1], r2 = c_views[3 * it + 2];
+    if (h.z == MODE_FAST) {
+      const uint32_t sbase = box_base + uint32_t(s * box_elems) * 4u;
+      if (CIRC) {
+        // P[0][2] == P[2][2] == 0: u and 1/w^2 are constant along z and v is
+        // affine in z (SURVEY §7 hard part (b)).
+        const float hx = fmaf(r0.x, x, fmaf(r0.y, y, r0.w));
+        const float hy = fmaf(r1.x, x, fmaf(r1.y, y, r1.w));
+        const float hz = fmaf(r2.x, x, fmaf(r2.y, y, r2.w));
+        const float r = __frcp_rn(hz);
+        const float invw2 = a.sid2 * r * r;
+        const float u = fmaf(hx, r, -float(h.x));
+        const float fu = floorf(u);
+        const float wu = u - fu;
+        const float p6r = r1.z * r;
+        const float v0 = fmaf(p6r, zf0, fmaf(hy, r, -float(h.y)));
+        const float dv = p6r * dz;
+        const uint32_t cbase = sbase + uint32_t(int(fu)) * 4u - MAGIC_BITS * ROWB;
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          const float vk = fmaf(float(min(k, kmax)), dv, v0);
+          const float t = __fadd_rd(vk, MAGIC);
+          const float wv = vk - (t - MAGIC);
+          const uint32_t ad = cbase + __float_as_uint(t) * ROWB;
+          const float a0 = lds_f32(ad), a1 = lds_f32(ad + 4);
+          const float b0 = lds_f32(ad + ROWB), b1 = lds_f32(ad + ROWB + 4);
+          const float top = fmaf(wu, a1 - a0, a0);
+          const float bot = fmaf(wu, b1 - b0, b0);
+          acc[k] = fmaf(fmaf(wv, bot - top, top), invw2, acc[k]);
+        }
+      } else {
+        // general calibrated matrices: full projective map per voxel
+        const float hx0 = fmaf(r0.x, x, fmaf(r0.y, y, r0.w));
+        const float hy0 = fmaf(r1.x, x, fmaf(r1.y, y, r1.w));
+        const float hz0 = fmaf(r2.x, x, fmaf(r2.y, y, r2.w));
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          const float z = fmaf(float(min(k, kmax)), dz, zf0);
+          const float hz = fmaf(r2.z, z, hz0);
+          const float r = __frcp_rn(hz);
+          const float u = fmaf(fmaf(r0.z, z, hx0), r, -float(h.x));
+          const float vk = fmaf(fmaf(r1.z, z, hy0), r, -float(h.y));
+          const float tu = __fadd_rd(u, MAGIC);
+          const float tv = __fadd_rd(vk, MAGIC);
+          const float wu = u - (tu - MAGIC);
+          const float wv = vk - (tv - MAGIC);
+          const uint32_t ad = sbase + (__float_as_uint(tu) - MAGIC_BITS) * 4u +
+                              (__float_as_uint(tv) - MAGIC_BITS) * ROWB;
+          const float a0 = lds_f32(ad), a1 = lds_f32(ad + 4);
+          const float b0 = lds_f32(ad + ROWB), b1 = lds_f32(ad + ROWB + 4);
+          const float top = fmaf(wu, a1 - a0, a0);
+          const float bot = fmaf(wu, b1 - b0, b0);
+          acc[k] = fmaf(fmaf(wv, bot - top, top), a.sid2 * r * r, acc[k]);
+        }
+      }
+    } else if (h.z == MODE_SLOW) {
+      const float* img = a.sino + (long long)(a.view_base + it) * a.view_pitch;
+#pragma unroll
+      for (int k = 0; k < K; ++k) {  // unrolled: acc[] must stay in registers
+        const float z = fmaf(float(min(k, kmax)), dz, zf0);
+        float u, v, hz;
+        project_point(r0, r1, r2, x, y, z, u, v, hz);
+        if (!(hz > 0.0f) || !(fabsf(u) < 4.0e6f) || !(fabsf(v) < 4.0e6f)) continue;
+        acc[k] += bilinear_global(a, img, u, v) * (a.sid2 / (hz * hz));
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+
+  if (!valid) return;
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    if (k > kmax) break;
+    float* o = a.vol + ((long long)(zt0 + k) * a.ny + iy) * a.nx + ix;
+    const float val = acc[k] * a.scale;
+    *o = a.accumulate ? *o + val : val;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K2: ray-driven forward projection
+
+struct FpArgs {
+  int nu, nv;
+  int view0;
+  int nx, ny, nz;
+  double ox, oy, oz, sx, sy, sz;
+  double step;                    // march_step: 0.5 * min pitch
+  const double* __restrict__ geo;  // per view: source (3) + inverse block (9)
+  const float* __restrict__ vpad;  // zero-bordered volume, +2 on each side
+  int nxp, nyp;                   // padded extents (x, y)
+  float* out;                     // [n_views][nv][nu]
+};
+
+#define DADD __dadd_rn
+#define DMUL __dmul_rn
+#define DDIV __ddiv_rn
+
+// projector.hpp:83-101 clip_ray in IEEE FP64 without contraction: the hit
+// test and the sample count are bit-exact with the reference.
+__device__ __forceinline__ bool clip_ray3(const FpArgs& a, const double o[3], const double d[3],
+                                          double& t0, double& t1) {
+  const double org[3] = {a.ox, a.oy, a.oz};
+  const double sp[3] = {a.sx, a.sy, a.sz};
+  const int n[3] = {a.nx, a.ny, a.nz};
+  t0 = -1e300;
+  t1 = 1e300;
+#pragma unroll
+  for (int ax = 0; ax < 3; ++ax) {
+    const double lo = DADD(org[ax], -sp[ax]);
+    const double hi = DADD(org[ax], DMUL(double(n[ax]), sp[ax]));
+    if (fabs(d[ax]) < 1e-12) {
+      if (o[ax] <= lo || o[ax] >= hi) return false;
+      continue;
+    }
+    double ta = DDIV(DADD(lo, -o[ax]), d[ax]);
+    double tb = DDIV(DADD(hi, -o[ax]), d[ax]);
+    if (ta > tb) {
+      const double tt = ta;
+      ta = tb;
+      tb = tt;
+    }
+    t0 = (t0 < ta) ? ta : t0;
+    t1 = (tb < t1) ? tb : t1;
+  }
+  return t1 > t0;
+}
+
+__device__ __forceinline__ float lerpf(float a, float b, float w) { return fmaf(w, b - a, a); }
+
+__global__ void __launch_bounds__(256) cone_fp_kernel(const FpArgs a) {
+  const int iu = blockIdx.x * 32 + threadIdx.x;
+  const int iv = blockIdx.y * 8 + threadIdx.y;
+  const int vl = blockIdx.z;
+  if (iu >= a.nu || iv >= a.nv) return;
+  const double* g = a.geo + 12 * (a.view0 + vl);
+  const double o[3] = {g[0], g[1], g[2]};
+  const double* M = g + 3;
+  // projector.hpp:275-277: d = M^-1 (iu, iv, 1), then (1/|d|) d
+  const double X = double(iu), Y = double(iv);
+  double d[3];
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+    d[r] = DADD(DADD(DMUL(M[3 * r], X), DMUL(M[3 * r + 1], Y)), DMUL(M[3 * r + 2], 1.0));
+  const double nn = DADD(DADD(DMUL(d[0], d[0]), DMUL(d[1], d[1])), DMUL(d[2], d[2]));
+  const double s = DDIV(1.0, __dsqrt_rn(nn));
+#pragma unroll
+  for (int r = 0; r < 3; ++r) d[r] = DMUL(s, d[r]);
+
+  float* out = a.out + ((long long)vl * a.nv + iv) * a.nu + iu;
+  double t0, t1;
+  if (!clip_ray3(a, o, d, t0, t1)) {
+    *out = 0.0f;
+    return;
+  }
+  const double span = DADD(t1, -t0);
+  const long long n = (long long)ceil(DDIV(span, a.step));
+  const double dt = DDIV(span, double(n));
+
+  // Sample k sits at t0 + (k + 1/2) dt; march in index space (fp32) from
+  // anchors recomputed in FP64 every 64 samples.
+  const double th = t0 + 0.5 * dt;
+  const double p0x = (o[0] + th * d[0] - a.ox) / a.sx + 2.0;
+  const double p0y = (o[1] + th * d[1] - a.oy) / a.sy + 2.0;
+  const double p0z = (o[2] + th * d[2] - a.oz) / a.sz + 2.0;
+  const double ddx = dt * d[0] / a.sx, ddy = dt * d[1] / a.sy, ddz = dt * d[2] / a.sz;
+  const float fdx = float(ddx), fdy = float(ddy), fdz = float(ddz);
+  const long long nxp = a.nxp, nxyp = (long long)a.nxp * a.nyp;
+  double total = 0.0;
+  for (long long k0 = 0; k0 < n; k0 += 64) {
+    const float bx = float(p0x + double(k0) * ddx);
+    const float by = float(p0y + double(k0) * ddy);
+    const float bz = float(p0z + double(k0) * ddz);
+    const int m = int(min(64LL, n - k0));
+    float sum = 0.0f;
+    for (int j = 0; j < m; ++j) {
+      const float px = fmaf(float(j), fdx, bx);
+      const float py = fmaf(float(j), fdy, by);
+      const float pz = fmaf(float(j), fdz, bz);
+      const float fx = floorf(px), fy = floorf(py), fz = floorf(pz);
+      const float wx = px - fx, wy = py - fy, wz = pz - fz;
+      const float* b = a.vpad + (long long)int(fz) * nxyp + (long long)int(fy) * nxp + int(fx);
+      const float c00 = lerpf(__ldg(b), __ldg(b + 1), wx);
+      const float c01 = lerpf(__ldg(b + nxp), __ldg(b + nxp + 1), wx);
+      const float c10 = lerpf(__ldg(b + nxyp), __ldg(b + nxyp + 1), wx);
+      const float c11 = lerpf(__ldg(b + nxyp + nxp), __ldg(b + nxyp + nxp + 1), wx);
+      sum += lerpf(lerpf(c00, c01, wy), lerpf(c10, c11, wy), wz);
+    }
+    total += double(sum);
+  }
+  *out = float(total * dt);
+}
+
+__global__ void pad_volume_kernel(const float* __restrict__ vol, float* __restrict__ vpad, int nx,
+                                  int ny, int nz) {
+  const int nxp = nx + 4, nyp = ny + 4, nzp = nz + 4;
+  const long long total = (long long)nxp * nyp * nzp;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int px = int(i % nxp);
+    const long long r = i / nxp;
+    const int py = int(r % nyp), pz = int(r / nyp);
+    const int x = px - 2, y = py - 2, z = pz - 2;
+    float v = 0.0f;
+    if (x >= 0 && x < nx && y >= 0 && y < ny && z >= 0 && z < nz)
+      v = __ldg(vol + ((long long)z * ny + y) * nx + x);
+    vpad[i] = v;
+  }
+}
+
+}  // namespace cone
+}  // namespace tgb
+
+// ===========================================================================
+// plan
+
+using namespace tgb;
+using namespace tgb::cone;
+
+struct tg_cone_plan {
+  int device = 0;
+  uint64_t id = 0;
+  tg_volume_spec vol{};
+  tg_detector2d det{};
+  uint64_t n_proj = 0;
+  double range = 0, sid = 0, sdd = 0;
+  std::vector<double> mats, sources, invs, angles;
+  bool circular = true;
+  float4* d_coef = nullptr;   // 3 x n_proj fp32 matrix rows
+  double* d_geo = nullptr;    // 12 x n_proj: source + inverse block (FP64)
+  int boxV = 0, boxU = 0;     // K1 TMA box
+  int need_w = 0, need_h = 0;
+  // FDK pre-processing
+  double* d_cos = nullptr;     // [n_v][n_u]
+  double* d_parker = nullptr;  // [n_proj][n_u]
+  filt::RowFilter* ramlak = nullptr;
+  // scratch
+  float* d_vpad = nullptr;
+  size_t vpad_elems = 0;
+  float* d_pitched = nullptr;  // band copy with a 16-byte row pitch when n_u % 4 != 0
+  size_t pitched_elems = 0;
+  std::mutex mu;
+};
+
+namespace {
+
+constexpr int kK = 16;  // z voxels per K1 thread
+
+int pick_boxu(int need) {
+  static const int choices[] = {16, 48, 80, 112, 144, 176, 208, 240};
+  for (int c : choices)
+    if (need <= c) return c;
+  return 240;
+}
+
+void cone_args_base(const tg_cone_plan& p, BpArgs& a) {
+  std::memset(&a, 0, sizeof a);
+  a.nx = int(p.vol.shape[0]);
+  a.ny = int(p.vol.shape[1]);
+  a.nz = int(p.vol.shape[2]);
+  a.ox = p.vol.origin[0];
+  a.oy = p.vol.origin[1];
+  a.oz = p.vol.origin[2];
+  a.sx = p.vol.spacing[0];
+  a.sy = p.vol.spacing[1];
+  a.sz = p.vol.spacing[2];
+  a.nu = int(p.det.n_u);
+  a.nv = int(p.det.n_v);
+  a.sid2 = float(p.sid * p.sid);
+}
+
+template <int K, int BOXU, bool CIRC>
+void launch_bp_t(const CUtensorMap& map, const BpArgs& a, size_t smem, cudaStream_t st) {
+  auto fn = cone_bp_kernel<K, BOXU, CIRC>;
+  TG_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  dim3 grid((a.nx + BX - 1) / BX, (a.ny + BY - 1) / BY, (a.nz + K - 1) / K);
+  fn<<<grid, NTHREADS, smem, st>>>(map, a);
+}
+
+template <bool CIRC>
+void launch_bp_u(int boxU, const CUtensorMap& map, const BpArgs& a, size_t smem, cudaStream_t st) {
+  switch (boxU) {
+    case 16: return launch_bp_t<kK, 16, CIRC>(map, a, smem, st);
+    case 48: return launch_bp_t<kK, 48, CIRC>(map, a, smem, st);
+    case 80: return launch_bp_t<kK, 80, CIRC>(map, a, smem, st);
+    case 112: return launch_bp_t<kK, 112, CIRC>(map, a, smem, st);
+    case 144: return launch_bp_t<kK, 144, CIRC>(map, a, smem, st);
+    case 176: return launch_bp_t<kK, 176, CIRC>(map, a, smem, st);
+    case 208: return launch_bp_t<kK, 208, CIRC>(map, a, smem, st);
+    default: return launch_bp_t<kK, 240, CIRC>(map, a, smem, st);
+  }
+}
+
+// Size K1's box from the real footprints of every (tile, view).
+void size_box(tg_cone_plan& p) {
+  BpArgs a;
+  cone_args_base(p, a);
+  a.n_views = int(p.n_proj);
+  const int tx = (a.nx + BX - 1) / BX, ty = (a.ny + BY - 1) / BY, tz = (a.nz + kK - 1) / kK;
+  int* d_need = nullptr;
+  TG_CUDA(cudaMalloc(&d_need, 2 * sizeof(int)));
+  TG_CUDA(cudaMemset(d_need, 0, 2 * sizeof(int)));
+  const long long total = (long long)tx * ty * tz * a.n_views;
+  const int threads = 256;
+  const long long blocks = (total + threads - 1) / threads;
+  footprint_kernel<<<unsigned(blocks), threads>>>(a, kK, tx, ty, tz, p.d_coef, d_need);
+  TG_LAUNCHED(1);
+  int need[2] = {0, 0};
+  TG_CUDA(cudaMemcpy(need, d_need, sizeof need, cudaMemcpyDeviceToHost));
+  TG_CUDA(cudaFree(d_need));
+  p.need_w = need[0];
+  p.need_h = need[1];
+  p.boxU = pick_boxu(std::max(need[0], 1));
+  p.boxV = std::min(std::max(need[1], 2), 256);
+  // keep the stage ring within ~96 KB so two CTAs fit per SM
+  while (p.boxV > 2 && size_t(STAGES) * p.boxU * p.boxV * 4 > 96 * 1024) --p.boxV;
+}
+
+// Back-project views [view0, view0 + n_views) of the band buffer (which holds
+// every view) into the slab.
+void backproject_impl(tg_cone_plan& p, uint64_t z0, uint64_t nz, uint64_t v0, uint64_t n_rows,
+                      const float* d_band, float* d_slab, float scale, int accumulate,
+                      cudaStream_t st, uint64_t view0 = 0, uint64_t n_views = ~0ull) {
+  if (n_views == ~0ull) n_views = p.n_proj - view0;
+  check(view0 + n_views <= p.n_proj && n_views >= 1, "view range lies outside the geometry");
+  check(z0 + nz <= p.vol.shape[2] && nz >= 1, "slab lies outside the volume");
+  check(n_rows >= 1 && v0 + n_rows <= p.det.n_v, "detector row band lies outside the detector");
+  DeviceGuard dg(p.device);
+  const uint64_t nu = p.det.n_u;
+  // TMA needs 16-byte aligned rows: re-pitch the band when n_u % 4 != 0
+  const float* src = d_band;
+  uint64_t pitch = nu;
+  if ((nu % 4) != 0 || (reinterpret_cast<uintptr_t>(d_band) % 16) != 0) {
+    pitch = (nu + 3) / 4 * 4;
+    const size_t need = size_t(pitch) * n_rows * p.n_proj;
+    std::lock_guard<std::mutex> lk(p.mu);
+    if (p.pitched_elems < need) {
+      if (p.d_pitched) TG_CUDA(cudaFree(p.d_pitched));
+      TG_CUDA(cudaMalloc(&p.d_pitched, need * sizeof(float)));
+      p.pitched_elems = need;
+    }
+    TG_CUDA(cudaMemcpy2DAsync(p.d_pitched, pitch * 4, d_band, nu * 4, nu * 4, n_rows * p.n_proj,
+                              cudaMemcpyDeviceToDevice, st));
+    src = p.d_pitched;
+  }
+  CUtensorMap map;
+  const CUresult cr = encode_tensor_map_3d_f32(&map, src, nu, n_rows, p.n_proj, pitch * 4,
+                                               pitch * n_rows * 4, uint32_t(p.boxU),
+                                               uint32_t(p.boxV));
+  if (cr != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed (" + std::to_string(int(cr)) + ")");
+
+  BpArgs a;
+  cone_args_base(p, a);
+  a.nz = int(nz);
+  a.z0 = int(z0);
+  a.band_v0 = int(v0);
+  a.band_rows = int(n_rows);
+  a.boxU = p.boxU;
+  a.boxV = p.boxV;
+  a.sino = src;
+  a.row_pitch = (long long)pitch;
+  a.view_pitch = (long long)(pitch * n_rows);
+  a.vol = d_slab;
+  const size_t smem = size_t(STAGES) * p.boxU * p.boxV * 4 + STAGES * sizeof(int4) +
+                      2 * STAGES * sizeof(uint64_t);
+  KernelTimer timer;
+  timer.start(st);
+  for (uint64_t c0 = view0; c0 < view0 + n_views; c0 += kMaxConstViews) {
+    const uint64_t cn = std::min<uint64_t>(kMaxConstViews, view0 + n_views - c0);
+    a.n_views = int(cn);
+    a.view_base = int(c0);
+    a.scale = scale;
+    a.accumulate = (c0 == view0) ? accumulate : 1;
+    std::lock_guard<std::mutex> lk(g_bank.mu);
+    // bank content key: (plan, first view, view count)
+    g_bank.acquire(p.device, (p.id << 40) ^ (c0 << 20) ^ cn, st, c_views, p.d_coef + 3 * c0,
+                   cn * 3 * sizeof(float4));
+    if (p.circular) launch_bp_u<true>(p.boxU, map, a, smem, st);
+    else launch_bp_u<false>(p.boxU, map, a, smem, st);
+    TG_LAUNCHED(1);
+    g_bank.release(p.device, st);
+  }
+  timer.stop();
+}
+
+void ensure_vpad(tg_cone_plan& p) {
+  const size_t need = size_t(p.vol.shape[0] + 4) * (p.vol.shape[1] + 4) * (p.vol.shape[2] + 4);
+  if (p.vpad_elems >= need) return;
+  if (p.d_vpad) TG_CUDA(cudaFree(p.d_vpad));
+  TG_CUDA(cudaMalloc(&p.d_vpad, need * sizeof(float)));
+  p.vpad_elems = need;
+}
+
+void forward_impl(tg_cone_plan& p, uint64_t view0, uint64_t nviews, const float* d_vol,
+                  float* d_out, cudaStream_t st, bool pad = true) {
+  check(view0 + nviews <= p.n_proj && nviews >= 1, "view range lies outside the geometry");
+  DeviceGuard dg(p.device);
+  std::lock_guard<std::mutex> lk(p.mu);
+  ensure_vpad(p);
+  const int nx = int(p.vol.shape[0]), ny = int(p.vol.shape[1]), nz = int(p.vol.shape[2]);
+  if (pad) {
+    pad_volume_kernel<<<148 * 8, 256, 0, st>>>(d_vol, p.d_vpad, nx, ny, nz);
+    TG_LAUNCHED(1);
+  }
+  FpArgs a;
+  a.nu = int(p.det.n_u);
+  a.nv = int(p.det.n_v);
+  a.nx = nx;
+  a.ny = ny;
+  a.nz = nz;
+  a.ox = p.vol.origin[0];
+  a.oy = p.vol.origin[1];
+  a.oz = p.vol.origin[2];
+  a.sx = p.vol.spacing[0];
+  a.sy = p.vol.spacing[1];
+  a.sz = p.vol.spacing[2];
+  double m = a.sx;  // projector.hpp:103-107
+  m = (a.sy < m) ? a.sy : m;
+  m = (a.sz < m) ? a.sz : m;
+  a.step = 0.5 * m;
+  a.geo = p.d_geo;
+  a.vpad = p.d_vpad;
+  a.nxp = nx + 4;
+  a.nyp = ny + 4;
+  KernelTimer timer;
+  timer.start(st);
+  // one launch per <= 65535 views (grid z limit)
+  for (uint64_t c0 = 0; c0 < nviews; c0 += 65535) {
+    const uint64_t cn = std::min<uint64_t>(65535, nviews - c0);
+    a.view0 = int(view0 + c0);
+    a.out = d_out + c0 * p.det.n_u * p.det.n_v;
+    dim3 grid((a.nu + 31) / 32, (a.nv + 7) / 8, unsigned(cn));
+    cone_fp_kernel<<<grid, dim3(32, 8), 0, st>>>(a);
+    TG_LAUNCHED(1);
+  }
+  timer.stop();
+}
+
+void ensure_fdk_weights(tg_cone_plan& p, bool use_parker) {
+  tg_cone_geometry g{p.vol, p.det, p.n_proj, p.range, p.sid, p.sdd, p.mats.data(), p.sources.data(),
+                     p.invs.data(), p.angles.data()};
+  std::lock_guard<std::mutex> lk(p.mu);
+  if (!p.d_cos) {
+    std::vector<double> cw(p.det.n_u * p.det.n_v);
+    cosine_weights_cone(g, cw.data());
+    TG_CUDA(cudaMalloc(&p.d_cos, cw.size() * sizeof(double)));
+    TG_CUDA(cudaMemcpy(p.d_cos, cw.data(), cw.size() * sizeof(double), cudaMemcpyHostToDevice));
+  }
+  if (use_parker && !p.d_parker) {
+    std::vector<double> pw(p.n_proj * p.det.n_u);
+    parker_weights_cone(g, pw.data());  // throws the reference's range errors
+    TG_CUDA(cudaMalloc(&p.d_parker, pw.size() * sizeof(double)));
+    TG_CUDA(cudaMemcpy(p.d_parker, pw.data(), pw.size() * sizeof(double), cudaMemcpyHostToDevice));
+  }
+  if (!p.ramlak) {
+    const uint64_t P = next_pow2(2 * p.det.n_u);
+    std::vector<double> w(P);
+    ramlak_weights(P, p.det.spacing_u, w.data());
+    p.ramlak = filt::create(p.det.n_u, P, w.data(), p.device);
+  }
+}
+
+void prefilter_impl(tg_cone_plan& p, const float* d_in, float* d_out, bool use_parker, uint64_t v0,
+                    uint64_t n_rows, uint64_t view0, uint64_t n_views, cudaStream_t st) {
+  check(n_rows >= 1 && v0 + n_rows <= p.det.n_v, "detector row band lies outside the detector");
+  ensure_fdk_weights(p, use_parker);
+  DeviceGuard dg(p.device);
+  filt::PreWeights pw;
+  pw.cos = p.d_cos;
+  pw.cos_row0 = v0;
+  pw.rows_per_view = n_rows;
+  pw.parker = use_parker ? p.d_parker + view0 * p.det.n_u : nullptr;
+  filt::apply(*p.ramlak, d_in, d_out, n_views * n_rows, &pw, st);
+}
+
+double fdk_scale(const tg_cone_plan& p, bool use_parker) {  // pipelines.hpp:80-81
+  return p.range / double(p.n_proj) * (p.sdd / p.sid) * (use_parker ? 1.0 : 0.5);
+}
+
+// Host-buffer pipelines: views in chunks, H2D on a copy stream overlapped with
+// the kernels of the previous chunk.  Staging buffers are per call.
+struct HostPipe {
+  cudaStream_t cs = nullptr, xs = nullptr;
+  std::vector<cudaEvent_t> ev;
+  explicit HostPipe(int n_events) {
+    TG_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    TG_CUDA(cudaStreamCreateWithFlags(&xs, cudaStreamNonBlocking));
+    ev.resize(n_events);
+    for (auto& e : ev) TG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  ~HostPipe() {
+    for (auto& e : ev) cudaEventDestroy(e);
+    cudaStreamDestroy(cs);
+    cudaStreamDestroy(xs);
+  }
+};
+
+void host_backproject(tg_cone_plan& p, const float* h_sino, float* h_vol, int fdk, bool use_parker) {
+  DeviceGuard dg(p.device);
+  const uint64_t nu = p.det.n_u, nv = p.det.n_v, np = p.n_proj;
+  const uint64_t per_view = nu * nv;
+  const uint64_t nvox = p.vol.shape[0] * p.vol.shape[1] * p.vol.shape[2];
+  if (fdk) ensure_fdk_weights(p, use_parker);
+  // ~8 chunks of views (multiple of the constant bank size never needed here)
+  const uint64_t chunk = std::max<uint64_t>(1, (np + 7) / 8);
+  const int n_chunks = int((np + chunk - 1) / chunk);
+  float *d_sino = nullptr, *d_vol = nullptr;
+  TG_CUDA(cudaMalloc(&d_sino, np * per_view * sizeof(float)));
+  TG_CUDA(cudaMalloc(&d_vol, nvox * sizeof(float)));
+  HostPipe hp(n_chunks);
+  const float scale = fdk ? float(fdk_scale(p, use_parker)) : 1.0f;
+  for (int c = 0; c < n_chunks; ++c) {
+    const uint64_t v0 = uint64_t(c) * chunk, vn = std::min(chunk, np - v0);
+    TG_CUDA(cudaMemcpyAsync(d_sino + v0 * per_view, h_sino + v0 * per_view,
+                            vn * per_view * sizeof(float), cudaMemcpyHostToDevice, hp.xs));
+    TG_CUDA(cudaEventRecord(hp.ev[c], hp.xs));
+  }
+  // K3 + K1 per chunk on the compute stream as chunks land; K1 accumulates
+  // chunk after chunk into the volume
+  for (int c = 0; c < n_chunks; ++c) {
+    const uint64_t v0 = uint64_t(c) * chunk, vn = std::min(chunk, np - v0);
+    TG_CUDA(cudaStreamWaitEvent(hp.cs, hp.ev[c], 0));
+    float* part = d_sino + v0 * per_view;
+    if (fdk) prefilter_impl(p, part, part, use_parker, 0, nv, v0, vn, hp.cs);
+    backproject_impl(p, 0, p.vol.shape[2], 0, nv, d_sino, d_vol, scale, c > 0, hp.cs, v0, vn);
+  }
+  TG_CUDA(cudaMemcpyAsync(h_vol, d_vol, nvox * sizeof(float), cudaMemcpyDeviceToHost, hp.cs));
+  TG_CUDA(cudaStreamSynchronize(hp.cs));
+  TG_CUDA(cudaFree(d_sino));
+  TG_CUDA(cudaFree(d_vol));
+}
+
+// Detector rows a z-slab can touch: project the slab's 8 corners on every
+// view (FP64).  For w > 0 the projective image of the box lies in their hull;
+// keep taps floor(v), floor(v)+1 plus one row of margin on each side.
+void slab_rows(const tg_cone_geometry& g, uint64_t z0, uint64_t nz, uint64_t* v0,
+               uint64_t* n_rows) {
+  const tg_volume_spec& vol = g.volume;
+  check(z0 + nz <= vol.shape[2] && nz >= 1, "slab lies outside the volume");
+  double vmin = 1e300, vmax = -1e300;
+  bool behind = false;
+  const double xs[2] = {vol.origin[0], vol.origin[0] + double(vol.shape[0] - 1) * vol.spacing[0]};
+  const double ys[2] = {vol.origin[1], vol.origin[1] + double(vol.shape[1] - 1) * vol.spacing[1]};
+  const double zs[2] = {vol.origin[2] + double(z0) * vol.spacing[2],
+                        vol.origin[2] + double(z0 + nz - 1) * vol.spacing[2]};
+  for (uint64_t i = 0; i < g.n_projections; ++i) {
+    const double* m = g.matrices + 12 * i;
+    for (int c = 0; c < 8; ++c) {
+      const double x = xs[c & 1], y = ys[(c >> 1) & 1], z = zs[c >> 2];
+      const double hy = m[4] * x + m[5] * y + m[6] * z + m[7];
+      const double hz = m[8] * x + m[9] * y + m[10] * z + m[11];
+      if (!(hz > 0.0)) {
+        behind = true;
+        continue;
+      }
+      vmin = std::min(vmin, hy / hz);
+      vmax = std::max(vmax, hy / hz);
+    }
+  }
+  long long lo = 0, hi = (long long)g.detector.n_v - 1;
+  if (!behind) {
+    lo = std::max<long long>(0, (long long)std::floor(vmin) - 1);
+    hi = std::min<long long>((long long)g.detector.n_v - 1, (long long)std::floor(vmax) + 2);
+  }
+  if (hi < lo) {  // the slab never reaches the detector: keep a single row
+    lo = 0;
+    hi = 0;
+  }
+  *v0 = uint64_t(lo);
+  *n_rows = uint64_t(hi - lo + 1);
+}
+
+}  // namespace
+
+extern "C" {
+
+tg_status tg_cone_plan_create(const tg_cone_geometry* g, int device, tg_cone_plan** out) {
+  return guarded([&] {
+    *out = nullptr;
+    validate_volume(g->volume);
+    check(g->volume.dims == 3, "cone beam geometry expects a 3D volume");
+    check(g->sid > 0.0 && g->sdd > g->sid, "cone beam requires 0 < SID < SDD");
+    check(g->n_projections >= 1, "need at least one projection");
+    check(g->detector.n_u >= 1 && g->detector.n_v >= 1,
+          "detector needs at least one pixel per axis");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+      cudaGetLastError();
+      throw CudaError("no CUDA device visible: the B200 path has no CPU fallback");
+    }
+    check(device >= 0 && device < ndev, "device index out of range");
+    auto p = std::make_unique<tg_cone_plan>();
+    p->device = device;
+    p->id = next_plan_id();
+    p->vol = g->volume;
+    p->det = g->detector;
+    p->n_proj = g->n_projections;
+    p->range = g->angular_range;
+    p->sid = g->sid;
+    p->sdd = g->sdd;
+    const uint64_t n = g->n_projections;
+    p->mats.assign(g->matrices, g->matrices + 12 * n);
+    p->sources.assign(g->sources, g->sources + 3 * n);
+    p->invs.assign(g->inv_blocks, g->inv_blocks + 9 * n);
+    p->angles.assign(g->angles, g->angles + n);
+    std::vector<float4> coef(3 * n);
+    std::vector<double> geo(12 * n);
+    for (uint64_t i = 0; i < n; ++i) {
+      const double* m = g->matrices + 12 * i;
+      if (m[2] != 0.0 || m[10] != 0.0) p->circular = false;
+      for (int r = 0; r < 3; ++r)
+        coef[3 * i + r] = make_float4(float(m[4 * r]), float(m[4 * r + 1]), float(m[4 * r + 2]),
+                                      float(m[4 * r + 3]));
+      for (int k = 0; k < 3; ++k) geo[12 * i + k] = g->sources[3 * i + k];
+      for (int k = 0; k < 9; ++k) geo[12 * i + 3 + k] = g->inv_blocks[9 * i + k];
+    }
+    DeviceGuard dg(device);
+    TG_CUDA(cudaMalloc(&p->d_coef, coef.size() * sizeof(float4)));
+    TG_CUDA(cudaMemcpy(p->d_coef, coef.data(), coef.size() * sizeof(float4), cudaMemcpyHostToDevice));
+    TG_CUDA(cudaMalloc(&p->d_geo, geo.size() * sizeof(double)));
+    TG_CUDA(cudaMemcpy(p->d_geo, geo.data(), geo.size() * sizeof(double), cudaMemcpyHostToDevice));
+    size_box(*p);
+    *out = p.release();
+  });
+}
+
+tg_status tg_cone_plan_destroy(tg_cone_plan* p) {
+  return guarded([&] {
+    if (!p) return;
+    g_bank.forget(p->id);
+    DeviceGuard dg(p->device);
+    cudaFree(p->d_coef);
+    cudaFree(p->d_geo);
+    cudaFree(p->d_cos);
+    cudaFree(p->d_parker);
+    cudaFree(p->d_vpad);
+    cudaFree(p->d_pitched);
+    if (p->ramlak) filt::destroy(p->ramlak);
+    delete p;
+  });
+}
+
+tg_status tg_cone_forward(tg_cone_plan* p, const float* d_vol, float* d_sino, void* stream) {
+  return guarded([&] { forward_impl(*p, 0, p->n_proj, d_vol, d_sino, as_stream(stream)); });
+}
+
+tg_status tg_cone_forward_views(tg_cone_plan* p, uint64_t view0, uint64_t n_views,
+                                const float* d_vol, float* d_part, void* stream) {
+  return guarded([&] { forward_impl(*p, view0, n_views, d_vol, d_part, as_stream(stream)); });
+}
+
+tg_status tg_cone_backproject(tg_cone_plan* p, const float* d_sino, float* d_vol, float scale,
+                              int accumulate, void* stream) {
+  return guarded([&] {
+    backproject_impl(*p, 0, p->vol.shape[2], 0, p->det.n_v, d_sino, d_vol, scale, accumulate,
+                     as_stream(stream));
+  });
+}
+
+tg_status tg_cone_slab_rows(tg_cone_plan* p, uint64_t z0, uint64_t nz, uint64_t* v0,
+                            uint64_t* n_rows) {
+  return guarded([&] {
+    tg_cone_geometry g{p->vol, p->det, p->n_proj, p->range, p->sid, p->sdd, p->mats.data(),
+                       p->sources.data(), p->invs.data(), p->angles.data()};
+    slab_rows(g, z0, nz, v0, n_rows);
+  });
+}
+
+tg_status tg_cone_slab_rows_geom(const tg_cone_geometry* g, uint64_t z0, uint64_t nz, uint64_t* v0,
+                                 uint64_t* n_rows) {
+  return guarded([&] { slab_rows(*g, z0, nz, v0, n_rows); });
+}
+
+tg_status tg_cone_backproject_slab(tg_cone_plan* p, uint64_t z0, uint64_t nz, uint64_t v0,
+                                   uint64_t n_rows, const float* d_band, float* d_slab, float scale,
+                                   int accumulate, void* stream) {
+  return guarded([&] {
+    backproject_impl(*p, z0, nz, v0, n_rows, d_band, d_slab, scale, accumulate, as_stream(stream));
+  });
+}
+
+tg_status tg_cone_fdk_prefilter(tg_cone_plan* p, const float* d_in, float* d_out, int use_parker,
+                                uint64_t v0, uint64_t n_rows, void* stream) {
+  return guarded([&] {
+    prefilter_impl(*p, d_in, d_out, use_parker != 0, v0, n_rows, 0, p->n_proj, as_stream(stream));
+  });
+}
+
+double tg_cone_fdk_scale(const tg_cone_plan* p, int use_parker) { return fdk_scale(*p, use_parker != 0); }
+
+tg_status tg_cone_fdk(tg_cone_plan* p, const float* d_sino, float* d_vol, float* d_work,
+                      int use_parker, void* stream) {
+  return guarded([&] {
+    cudaStream_t st = as_stream(stream);
+    prefilter_impl(*p, d_sino, d_work, use_parker != 0, 0, p->det.n_v, 0, p->n_proj, st);
+    backproject_impl(*p, 0, p->vol.shape[2], 0, p->det.n_v, d_work, d_vol,
+                     float(fdk_scale(*p, use_parker != 0)), 0, st);
+  });
+}
+
+tg_status tg_cone_forward_host(tg_cone_plan* p, const float* h_vol, float* h_sino) {
+  return guarded([&] {
+    DeviceGuard dg(p->device);
+    const uint64_t nvox = p->vol.shape[0] * p->vol.shape[1] * p->vol.shape[2];
+    const uint64_t per_view = p->det.n_u * p->det.n_v;
+    float *d_vol = nullptr, *d_sino = nullptr;
+    TG_CUDA(cudaMalloc(&d_vol, nvox * sizeof(float)));
+    TG_CUDA(cudaMalloc(&d_sino, p->n_proj * per_view * sizeof(float)));
+    HostPipe hp(1);
+    TG_CUDA(cudaMemcpyAsync(d_vol, h_vol, nvox * sizeof(float), cudaMemcpyHostToDevice, hp.cs));
+    // views in chunks so the D2H of chunk c overlaps the projection of c+1
+    const uint64_t chunk = std::max<uint64_t>(1, (p->n_proj + 7) / 8);
+    for (uint64_t v0 = 0; v0 < p->n_proj; v0 += chunk) {
+      const uint64_t vn = std::min(chunk, p->n_proj - v0);
+      forward_impl(*p, v0, vn, d_vol, d_sino + v0 * per_view, hp.cs, v0 == 0);
+      TG_CUDA(cudaEventRecord(hp.ev[0], hp.cs));
+      TG_CUDA(cudaStreamWaitEvent(hp.xs, hp.ev[0], 0));
+      TG_CUDA(cudaMemcpyAsync(h_sino + v0 * per_view, d_sino + v0 * per_view,
+                              vn * per_view * sizeof(float), cudaMemcpyDeviceToHost, hp.xs));
+    }
+    TG_CUDA(cudaStreamSynchronize(hp.xs));
+    TG_CUDA(cudaStreamSynchronize(hp.cs));
+    TG_CUDA(cudaFree(d_vol));
+    TG_CUDA(cudaFree(d_sino));
+  });
+}
+
+tg_status tg_cone_backproject_host(tg_cone_plan* p, const float* h_sino, float* h_vol) {
+  return guarded([&] { host_backproject(*p, h_sino, h_vol, 0, false); });
+}
+
+tg_status tg_cone_fdk_host(tg_cone_plan* p, const float* h_sino, float* h_vol, int use_parker) {
+  return guarded([&] { host_backproject(*p, h_sino, h_vol, 1, use_parker != 0); });
+}
+
+}  // extern "C"

@@ -1,0 +1,284 @@
+// filter.cu — K3 row filter: shared-memory Stockham FFT (radix 4, one
+// radix-2 tail when log2 P is odd), two real rows per complex transform when
+// the weights are symmetric, fused FDK pre-weights, fused truncation.
+//
+// The reference (filtering.hpp:95-110) zero-pads each row to P, runs a
+// complex-double FFT, multiplies by the real weights, inverse-transforms
+// and keeps the first n samples.  This kernel computes the same linear map
+// in fp32 with FP64-derived twiddles; parity tolerance is stated in
+// tests/test_gpu_filter.py.
+#include <cmath>
+#include <memory>
+#include <vector>
+
+#include "filter.cuh"
+
+namespace tgb {
+namespace filt {
+
+namespace {
+
+constexpr int kThreads = 256;
+
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+  return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ float2 conj_if(float2 a, bool inv) { return inv ? make_float2(a.x, -a.y) : a; }
+
+// One Stockham pass set over smem buffers x <-> y; returns the buffer holding
+// the result.  Twiddles w_P(m) = exp(-2 pi i m / P); the inverse conjugates.
+__device__ float2* fft_smem(float2* x, float2* y, int P, const float2* __restrict__ tw, bool inv) {
+  int Ns = 1;
+  const int q = P >> 2;
+  while (Ns * 4 <= P) {
+    for (int j = threadIdx.x; j < q; j += blockDim.x) {
+      const int k = j & (Ns - 1);
+      float2 v0 = x[j], v1 = x[j + q], v2 = x[j + 2 * q], v3 = x[j + 3 * q];
+      if (Ns > 1) {
+        const int m = k * (P / (4 * Ns));
+        v1 = cmul(v1, conj_if(__ldg(tw + m), inv));
+        v2 = cmul(v2, conj_if(__ldg(tw + 2 * m), inv));
+        v3 = cmul(v3, conj_if(__ldg(tw + 3 * m), inv));
+      }
+      const float2 a0 = cadd(v0, v2), a1 = csub(v0, v2), a2 = cadd(v1, v3);
+      const float2 d = csub(v1, v3);
+      // forward: -i*d, inverse: +i*d
+      const float2 a3 = inv ? make_float2(-d.y, d.x) : make_float2(d.y, -d.x);
+      const int o = (j - k) * 4 + k;
+      y[o] = cadd(a0, a2);
+      y[o + Ns] = cadd(a1, a3);
+      y[o + 2 * Ns] = csub(a0, a2);
+      y[o + 3 * Ns] = csub(a1, a3);
+    }
+    __syncthreads();
+    float2* t = x;
+    x = y;
+    y = t;
+    Ns *= 4;
+  }
+  if (Ns < P) {  // radix-2 tail, Ns == P / 2
+    const int h = P >> 1;
+    for (int j = threadIdx.x; j < h; j += blockDim.x) {
+      const float2 v0 = x[j];
+      const float2 v1 = cmul(x[j + h], conj_if(__ldg(tw + j), inv));
+      y[j] = cadd(v0, v1);
+      y[j + h] = csub(v0, v1);
+    }
+    __syncthreads();
+    x = y;
+  }
+  return x;
+}
+
+__device__ __forceinline__ float pre_weight(float v, const PreWeights& pw, uint64_t row, int j,
+                                            int n) {
+  if (pw.cos) {
+    const uint64_t vrow = pw.cos_row0 + row % pw.rows_per_view;
+    v = float(double(v) * __ldg(pw.cos + vrow * n + j));
+  }
+  if (pw.parker) {
+    const uint64_t view = row / pw.rows_per_view;
+    v = float(double(v) * __ldg(pw.parker + view * n + j));
+  }
+  return v;
+}
+
+// blockIdx.x -> rows (2b, 2b+1) when packed, row b otherwise
+__global__ void __launch_bounds__(kThreads) row_filter_kernel(const float* in, float* out, int n,
+                                                             int P, uint64_t n_rows, bool packed,
+                                                             const float* __restrict__ w,
+                                                             const float2* __restrict__ tw,
+                                                             PreWeights pw) {
+  extern __shared__ float2 buf[];
+  float2* x = buf;
+  float2* y = buf + P;
+  const uint64_t ra = packed ? 2 * uint64_t(blockIdx.x) : uint64_t(blockIdx.x);
+  const bool has_b = packed && ra + 1 < n_rows;
+  const float* pa = in + ra * uint64_t(n);
+  const float* pb = in + (ra + 1) * uint64_t(n);
+  for (int j = threadIdx.x; j < P; j += blockDim.x) {
+    float2 z = make_float2(0.f, 0.f);
+    if (j < n) {
+      z.x = pre_weight(pa[j], pw, ra, j, n);
+      if (has_b) z.y = pre_weight(pb[j], pw, ra + 1, j, n);
+    }
+    x[j] = z;
+  }
+  __syncthreads();
+  float2* X = fft_smem(x, y, P, tw, false);
+  float2* other = (X == x) ? y : x;
+  for (int k = threadIdx.x; k < P; k += blockDim.x) {
+    const float wk = __ldg(w + k);
+    X[k] = make_float2(X[k].x * wk, X[k].y * wk);
+  }
+  __syncthreads();
+  float2* Z = fft_smem(X, other, P, tw, true);
+  const float inv = 1.0f / float(P);
+  float* oa = out + ra * uint64_t(n);
+  float* ob = out + (ra + 1) * uint64_t(n);
+  for (int j = threadIdx.x; j < n; j += blockDim.x) {
+    oa[j] = Z[j].x * inv;
+    if (has_b) ob[j] = Z[j].y * inv;
+  }
+}
+
+__global__ void apply_weights_kernel(const float* in, float* out, uint64_t n, const double* map,
+                                     uint64_t map_n) {
+  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += uint64_t(gridDim.x) * blockDim.x)
+    out[i] = float(double(in[i]) * __ldg(map + i % map_n));
+}
+
+__global__ void apply_row_weights_kernel(const float* in, float* out, uint64_t total,
+                                         uint64_t n_rows, uint64_t n, const double* map) {
+  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t view = i / (n_rows * n), j = i % n;
+    out[i] = float(double(in[i]) * __ldg(map + view * n + j));
+  }
+}
+
+}  // namespace
+
+RowFilter* create(uint64_t n, uint64_t P, const double* weights, int device) {
+  check(P >= 2 && is_pow2(P), "filter window must be a power of two");
+  check(P <= 8192, "filter window exceeds the device filter's 8192-sample limit");
+  auto f = std::make_unique<RowFilter>();
+  f->device = device;
+  f->n = n;
+  f->P = P;
+  for (uint64_t k = 1; k < P; ++k)
+    if (weights[k] != weights[P - k]) f->symmetric = false;
+  std::vector<float> w(P);
+  for (uint64_t k = 0; k < P; ++k) w[k] = float(weights[k]);
+  std::vector<float2> tw(P);
+  for (uint64_t k = 0; k < P; ++k) {
+    const double ang = -2.0 * kPi * double(k) / double(P);
+    tw[k] = make_float2(float(std::cos(ang)), float(std::sin(ang)));
+  }
+  DeviceGuard dg(device);
+  TG_CUDA(cudaMalloc(&f->d_w, P * sizeof(float)));
+  TG_CUDA(cudaMalloc(&f->d_tw, P * sizeof(float2)));
+  TG_CUDA(cudaMemcpy(f->d_w, w.data(), P * sizeof(float), cudaMemcpyHostToDevice));
+  TG_CUDA(cudaMemcpy(f->d_tw, tw.data(), P * sizeof(float2), cudaMemcpyHostToDevice));
+  return f.release();
+}
+
+void destroy(RowFilter* f) {
+  if (!f) return;
+  cudaFree(f->d_w);
+  cudaFree(f->d_tw);
+  delete f;
+}
+
+void apply(const RowFilter& f, const float* d_in, float* d_out, uint64_t n_rows,
+           const PreWeights* pw, cudaStream_t st) {
+  if (n_rows == 0) return;
+  DeviceGuard dg(f.device);
+  PreWeights w = pw ? *pw : PreWeights{};
+  const bool packed = f.symmetric;
+  const uint64_t blocks = packed ? (n_rows + 1) / 2 : n_rows;
+  const size_t smem = 2 * f.P * sizeof(float2);
+  TG_CUDA(cudaFuncSetAttribute(row_filter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               int(smem)));
+  KernelTimer timer;
+  timer.start(st);
+  for (uint64_t b0 = 0; b0 < blocks; b0 += 2147483647ull) {
+    const uint64_t nb = std::min<uint64_t>(blocks - b0, 2147483647ull);
+    const uint64_t row0 = packed ? 2 * b0 : b0;
+    PreWeights wc = w;
+    // keep row numbering relative to this launch's first row
+    if (wc.parker) wc.parker += (row0 / wc.rows_per_view) * f.n;
+    row_filter_kernel<<<unsigned(nb), kThreads, smem, st>>>(
+        d_in + row0 * f.n, d_out + row0 * f.n, int(f.n), int(f.P), n_rows - row0, packed, f.d_w,
+        f.d_tw, wc);
+    TG_LAUNCHED(1);
+  }
+  timer.stop();
+}
+
+}  // namespace filt
+}  // namespace tgb
+
+// ---------------------------------------------------------------------------
+// C ABI
+
+using namespace tgb;
+
+struct tg_filter_plan {
+  filt::RowFilter* f = nullptr;
+};
+
+extern "C" {
+
+tg_status tg_filter_plan_create(uint64_t row_len, double row_spacing, uint64_t filt_n_bins,
+                                uint64_t padded_n, double filt_spacing, const double* weights,
+                                uint64_t n_weights, int device, tg_filter_plan** out) {
+  return guarded([&] {
+    *out = nullptr;
+    // filtering.hpp:117-121 then 97-99, in the reference's order
+    check(filt_n_bins == row_len, "filter was built for a different detector width");
+    check(std::abs(filt_spacing - row_spacing) <= 1e-12 * std::max(1.0, std::abs(row_spacing)),
+          "filter spacing does not match the detector spacing");
+    check(n_weights == padded_n && is_pow2(padded_n),
+          "filter window is inconsistent with its weight vector");
+    check(padded_n >= row_len, "filter window is smaller than the detector row");
+    auto p = std::make_unique<tg_filter_plan>();
+    p->f = filt::create(row_len, padded_n, weights, device);
+    *out = p.release();
+  });
+}
+
+tg_status tg_filter_plan_destroy(tg_filter_plan* p) {
+  return guarded([&] {
+    if (!p) return;
+    filt::destroy(p->f);
+    delete p;
+  });
+}
+
+tg_status tg_filter_apply(tg_filter_plan* p, const float* d_in, float* d_out, uint64_t n_rows,
+                          void* stream) {
+  return guarded([&] { filt::apply(*p->f, d_in, d_out, n_rows, nullptr, as_stream(stream)); });
+}
+
+tg_status tg_filter_apply_host(tg_filter_plan* p, const float* h_in, float* h_out, uint64_t n_rows) {
+  return guarded([&] {
+    DeviceGuard dg(p->f->device);
+    const size_t bytes = n_rows * p->f->n * sizeof(float);
+    float* d = nullptr;
+    TG_CUDA(cudaMalloc(&d, bytes ? bytes : 4));
+    TG_CUDA(cudaMemcpy(d, h_in, bytes, cudaMemcpyHostToDevice));
+    filt::apply(*p->f, d, d, n_rows, nullptr, 0);
+    TG_CUDA(cudaMemcpy(h_out, d, bytes, cudaMemcpyDeviceToHost));
+    TG_CUDA(cudaFree(d));
+  });
+}
+
+tg_status tg_apply_weights(const float* d_in, float* d_out, uint64_t n_total, const double* d_map,
+                           uint64_t map_n, void* stream) {
+  return guarded([&] {
+    check(map_n >= 1, "weight map shape matches neither the sinogram nor its detector");
+    if (n_total == 0) return;
+    const uint64_t blocks = std::min<uint64_t>((n_total + 255) / 256, 148 * 32);
+    filt::apply_weights_kernel<<<unsigned(blocks), 256, 0, as_stream(stream)>>>(d_in, d_out, n_total, d_map,
+                                                                         map_n);
+    TG_LAUNCHED(1);
+  });
+}
+
+tg_status tg_apply_row_weights(const float* d_in, float* d_out, uint64_t n_views, uint64_t n_rows,
+                               uint64_t n, const double* d_map, void* stream) {
+  return guarded([&] {
+    const uint64_t total = n_views * n_rows * n;
+    if (total == 0) return;
+    const uint64_t blocks = std::min<uint64_t>((total + 255) / 256, 148 * 32);
+    filt::apply_row_weights_kernel<<<unsigned(blocks), 256, 0, as_stream(stream)>>>(
+        d_in, d_out, total, n_rows, n, d_map);
+    TG_LAUNCHED(1);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,38 @@
+// filter.cuh — K3: row-wise frequency-domain filtering (Ram-Lak / ramp /
+// learned weights) with the FDK cosine and Parker weights fused into the
+// load.  Reference: filtering.hpp:95-125 (filter_rows / apply_filter),
+// 136-154 (apply_weights), fft.hpp:25-58 (the transform it replaces).
+#pragma once
+
+#include "device_common.cuh"
+
+namespace tgb {
+namespace filt {
+
+struct RowFilter {
+  int device = 0;
+  uint64_t n = 0;          // row length (detector bins)
+  uint64_t P = 0;          // power-of-two window
+  bool symmetric = true;   // W[k] == W[P-k]: two real rows share one complex FFT
+  float* d_w = nullptr;    // P real weights (fp32)
+  float2* d_tw = nullptr;  // P twiddles exp(-2 pi i k / P) (from FP64)
+};
+
+// Optional per-element weights applied (in FP64, rounded to fp32 after each
+// map, like the reference's two apply_weights passes) before filtering.
+// Row r of the launch is detector row cos_row0 + r % rows_per_view of view
+// r / rows_per_view.
+struct PreWeights {
+  const double* cos = nullptr;     // [n_v][n] (full detector)
+  uint64_t cos_row0 = 0;
+  uint64_t rows_per_view = 1;
+  const double* parker = nullptr;  // [views][n]
+};
+
+RowFilter* create(uint64_t n, uint64_t P, const double* weights, int device);
+void destroy(RowFilter* f);
+void apply(const RowFilter& f, const float* d_in, float* d_out, uint64_t n_rows,
+           const PreWeights* pw, cudaStream_t st);
+
+}  // namespace filt
+}  // namespace tgb
