@@ -13,75 +13,95 @@
 namespace tgb {
 namespace cone {
 
-__constant__ float4 c_views[3 * kMaxConstViews];
+// per-view projection matrices in FP64, row-major P = K[R|t] (12 doubles)
+__constant__ double c_views[12 * kMaxConstViews];
 static ConstBank g_bank;
 
 // ---------------------------------------------------------------------------
-// shared footprint logic (producer warp and plan-time sizing use the same
-// fp32 arithmetic)
+// Footprint + local frame of one (tile, view), computed in FP64 by the
+// producer warp (and, identically, by the plan-time sizing kernel).
 
-__device__ __forceinline__ Footprint make_footprint(float umin, float umax, float vmin, float vmax,
-                                                    bool ok, int nu, int nv) {
+__device__ __forceinline__ Footprint make_footprint(double umin, double umax, double vmin,
+                                                    double vmax, bool ok, int nu, int nv) {
   Footprint f;
-  ok = ok && fabsf(umin) < 4.0e6f && fabsf(umax) < 4.0e6f && fabsf(vmin) < 4.0e6f &&
-       fabsf(vmax) < 4.0e6f;
+  ok = ok && fabs(umin) < 4.0e6 && fabs(umax) < 4.0e6 && fabs(vmin) < 4.0e6 && fabs(vmax) < 4.0e6;
   f.ok = ok;
   if (!ok) {
     f.ub = f.vb = f.width = f.height = 0;
     f.hit = true;
     return f;
   }
-  const int u_lo = int(floorf(umin)), u_hi = int(floorf(umax));
-  const int v_lo = int(floorf(vmin)), v_hi = int(floorf(vmax));
-  f.ub = u_lo - 1;
+  const int u_lo = int(floor(umin)), u_hi = int(floor(umax));
+  const int v_lo = int(floor(vmin)), v_hi = int(floor(vmax));
+  // taps [u_lo, u_hi + 1] plus one pixel of margin each side; the box's
+  // first column is rounded down to a multiple of 4 because TMA requires
+  // 16-byte aligned inner coordinates
+  f.ub = (u_lo - 1) & ~3;
   f.vb = v_lo - 1;
-  f.width = u_hi - u_lo + 4;   // taps [u_lo, u_hi + 1] plus one pixel each side
+  f.width = u_hi + 3 - f.ub;
   f.height = v_hi - v_lo + 4;
   // every tap outside the detector contributes exactly zero
   f.hit = !(u_hi + 2 < 0 || f.ub > nu - 1 || v_hi + 2 < 0 || f.vb > nv - 1);
   return f;
 }
 
-struct TileBox {
-  float x[2], y[2], z[2];
+// Tile extent in voxel indices (slab-local z) and its centre in world units.
+struct Tile {
+  int x0, x1, y0, y1, z0, z1;  // inclusive
+  double xc, yc, zc;           // centre (mm)
 };
 
-__device__ __forceinline__ TileBox tile_corners(const BpArgs& a, int tx, int ty, int tz, int K) {
-  TileBox b;
-  const int x0 = tx * BX, y0 = ty * BY, z0 = tz * K;
-  const int x1 = min(x0 + BX, a.nx) - 1, y1 = min(y0 + BY, a.ny) - 1, z1 = min(z0 + K, a.nz) - 1;
-  b.x[0] = float(a.ox + double(x0) * a.sx);
-  b.x[1] = float(a.ox + double(x1) * a.sx);
-  b.y[0] = float(a.oy + double(y0) * a.sy);
-  b.y[1] = float(a.oy + double(y1) * a.sy);
-  b.z[0] = float(a.oz + double(a.z0 + z0) * a.sz);
-  b.z[1] = float(a.oz + double(a.z0 + z1) * a.sz);
-  return b;
+__device__ __forceinline__ Tile make_tile(const BpArgs& a, int tx, int ty, int tz, int K) {
+  Tile t;
+  t.x0 = tx * BX;
+  t.y0 = ty * BY;
+  t.z0 = tz * K;
+  t.x1 = min(t.x0 + BX, a.nx) - 1;
+  t.y1 = min(t.y0 + BY, a.ny) - 1;
+  t.z1 = min(t.z0 + K, a.nz) - 1;
+  t.xc = a.ox + 0.5 * double(t.x0 + t.x1) * a.sx;
+  t.yc = a.oy + 0.5 * double(t.y0 + t.y1) * a.sy;
+  t.zc = a.oz + 0.5 * double(2 * a.z0 + t.z0 + t.z1) * a.sz;
+  return t;
+}
+
+__device__ __forceinline__ void corner_uv(const double* P, const BpArgs& a, const Tile& t, int c,
+                                          double& u, double& v, bool& ok) {
+  const double x = a.ox + double((c & 1) ? t.x1 : t.x0) * a.sx;
+  const double y = a.oy + double((c & 2) ? t.y1 : t.y0) * a.sy;
+  const double z = a.oz + double(a.z0 + ((c & 4) ? t.z1 : t.z0)) * a.sz;
+  const double hx = P[0] * x + P[1] * y + P[2] * z + P[3];
+  const double hy = P[4] * x + P[5] * y + P[6] * z + P[7];
+  const double hz = P[8] * x + P[9] * y + P[10] * z + P[11];
+  ok = hz > 0.0;
+  u = hx / hz;
+  v = hy / hz;
 }
 
 // plan-time: largest footprint over every (tile, view) that takes the fast path
 __global__ void footprint_kernel(BpArgs a, int K, int tiles_x, int tiles_y, int tiles_z,
-                                 const float4* __restrict__ coef, int* __restrict__ need) {
+                                 const double* __restrict__ mats, int* __restrict__ need) {
   const long long n_tiles = (long long)tiles_x * tiles_y * tiles_z;
   const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= n_tiles * a.n_views) return;
   const int view = int(idx / n_tiles);
-  long long t = idx % n_tiles;
-  const int tx = int(t % tiles_x);
-  t /= tiles_x;
-  const int ty = int(t % tiles_y), tz = int(t / tiles_y);
-  const TileBox b = tile_corners(a, tx, ty, tz, K);
-  const float4 r0 = coef[3 * view], r1 = coef[3 * view + 1], r2 = coef[3 * view + 2];
-  float umin = INFINITY, umax = -INFINITY, vmin = INFINITY, vmax = -INFINITY;
+  long long r = idx % n_tiles;
+  const int tx = int(r % tiles_x);
+  r /= tiles_x;
+  const int ty = int(r % tiles_y), tz = int(r / tiles_y);
+  const Tile t = make_tile(a, tx, ty, tz, K);
+  const double* P = mats + 12 * view;
+  double umin = 1e300, umax = -1e300, vmin = 1e300, vmax = -1e300;
   bool ok = true;
   for (int c = 0; c < 8; ++c) {
-    float u, v, hz;
-    project_point(r0, r1, r2, b.x[c & 1], b.y[(c >> 1) & 1], b.z[c >> 2], u, v, hz);
-    ok = ok && hz > 0.0f;
-    umin = fminf(umin, u);
-    umax = fmaxf(umax, u);
-    vmin = fminf(vmin, v);
-    vmax = fmaxf(vmax, v);
+    double u, v;
+    bool okc;
+    corner_uv(P, a, t, c, u, v, okc);
+    ok = ok && okc;
+    umin = fmin(umin, u);
+    umax = fmax(umax, u);
+    vmin = fmin(vmin, v);
+    vmax = fmax(vmax, v);
   }
   const Footprint f = make_footprint(umin, umax, vmin, vmax, ok, a.nu, a.nv);
   if (f.ok && f.hit) {
@@ -120,13 +140,25 @@ __device__ __forceinline__ float bilinear_global(const BpArgs& a, const float* _
   return acc;
 }
 
+// Per-stage header written by the producer: the view's projective map in a
+// local frame, h = M (dx, dy, dz, 1) with (dx, dy, dz) the voxel's offset
+// from the tile centre and the u / v rows already shifted by the box origin
+// (u_row -= ub * w_row, v_row -= vb * w_row).  Built in FP64, so fp32
+// consumers see small, well-conditioned numbers.
+struct StageHdr {
+  float4 U, V, W;
+  int4 meta;  // ub, vb, mode, -
+};
+
 template <int K, int BOXU, bool CIRC>
 __global__ void __launch_bounds__(NTHREADS, 2)
     cone_bp_kernel(const __grid_constant__ CUtensorMap tmap, const BpArgs a) {
   extern __shared__ __align__(128) unsigned char smem[];
   const int box_elems = BOXU * a.boxV;
+  // TMA needs 128-byte aligned shared destinations: pad the stage stride
+  const int stage_elems = (box_elems + 31) & ~31;
   float* boxes = reinterpret_cast<float*>(smem);
-  int4* hdr = reinterpret_cast<int4*>(boxes + STAGES * box_elems);
+  StageHdr* hdr = reinterpret_cast<StageHdr*>(boxes + STAGES * stage_elems);
   uint64_t* full = reinterpret_cast<uint64_t*>(hdr + STAGES);
   uint64_t* empty = full + STAGES;
 
@@ -139,29 +171,27 @@ __global__ void __launch_bounds__(NTHREADS, 2)
     mbar_fence_init();
   }
   __syncthreads();
+  const Tile tile = make_tile(a, blockIdx.x, blockIdx.y, blockIdx.z, K);
 
   if (tid >= NCONS) {
-    // ---------------- producer warp: footprint + TMA per view -------------
+    // ---------------- producer warp: footprint, frame, TMA per view --------
     const int lane = tid & 31;
     if (lane == 0) prefetch_tensor_map(&tmap);
-    const TileBox b = tile_corners(a, blockIdx.x, blockIdx.y, blockIdx.z, K);
-    const float cx = (lane & 1) ? b.x[1] : b.x[0];
-    const float cy = (lane & 2) ? b.y[1] : b.y[0];
-    const float cz = (lane & 4) ? b.z[1] : b.z[0];
     for (int it = 0; it < a.n_views; ++it) {
       const int s = it % STAGES;
       if (it >= STAGES) mbar_wait(&empty[s], ((it / STAGES) - 1) & 1);
-      const float4 r0 = c_views[3 * it], r1 = c_views[3 * it + 1], r2 = c_views[3 * it + 2];
-      float u, v, hz;
-      project_point(r0, r1, r2, cx, cy, cz, u, v, hz);
-      bool ok = hz > 0.0f;
-      float umin = u, umax = u, vmin = v, vmax = v;
+      const double* P = c_views + 12 * it;
+      double u = 0.0, v = 0.0;
+      bool ok = true;
+      if (lane < 8) corner_uv(P, a, tile, lane, u, v, ok);
+      double umin = lane < 8 ? u : 1e300, umax = lane < 8 ? u : -1e300;
+      double vmin = lane < 8 ? v : 1e300, vmax = lane < 8 ? v : -1e300;
 #pragma unroll
       for (int off = 4; off >= 1; off >>= 1) {  // reduce over the 8 corner lanes
-        umin = fminf(umin, __shfl_xor_sync(0xffffffffu, umin, off));
-        umax = fmaxf(umax, __shfl_xor_sync(0xffffffffu, umax, off));
-        vmin = fminf(vmin, __shfl_xor_sync(0xffffffffu, vmin, off));
-        vmax = fmaxf(vmax, __shfl_xor_sync(0xffffffffu, vmax, off));
+        umin = fmin(umin, __shfl_xor_sync(0xffffffffu, umin, off));
+        umax = fmax(umax, __shfl_xor_sync(0xffffffffu, umax, off));
+        vmin = fmin(vmin, __shfl_xor_sync(0xffffffffu, vmin, off));
+        vmax = fmax(vmax, __shfl_xor_sync(0xffffffffu, vmax, off));
         ok = __shfl_xor_sync(0xffffffffu, int(ok), off) && ok;
       }
       if (lane == 0) {
@@ -169,10 +199,24 @@ __global__ void __launch_bounds__(NTHREADS, 2)
         int mode = MODE_SLOW;
         if (f.ok && !f.hit) mode = MODE_SKIP;
         else if (f.ok && f.width <= BOXU && f.height <= a.boxV) mode = MODE_FAST;
-        hdr[s] = make_int4(f.ub, f.vb, mode, 0);
+        // local frame: rows evaluated at the tile centre, u/v shifted to the box
+        const double ub = mode == MODE_FAST ? double(f.ub) : 0.0;
+        const double vb = mode == MODE_FAST ? double(f.vb) : 0.0;
+        double hc[3];
+#pragma unroll
+        for (int r = 0; r < 3; ++r)
+          hc[r] = P[4 * r] * tile.xc + P[4 * r + 1] * tile.yc + P[4 * r + 2] * tile.zc + P[4 * r + 3];
+        StageHdr h;
+        h.U = make_float4(float(P[0] - ub * P[8]), float(P[1] - ub * P[9]),
+                          float(P[2] - ub * P[10]), float(hc[0] - ub * hc[2]));
+        h.V = make_float4(float(P[4] - vb * P[8]), float(P[5] - vb * P[9]),
+                          float(P[6] - vb * P[10]), float(hc[1] - vb * hc[2]));
+        h.W = make_float4(float(P[8]), float(P[9]), float(P[10]), float(hc[2]));
+        h.meta = make_int4(f.ub, f.vb, mode, 0);
+        hdr[s] = h;
         if (mode == MODE_FAST) {
           mbar_arrive_expect_tx(&full[s], uint32_t(box_elems * 4));
-          tma_load_3d(boxes + s * box_elems, &tmap, &full[s], f.ub, f.vb - a.band_v0,
+          tma_load_3d(boxes + s * stage_elems, &tmap, &full[s], f.ub, f.vb - a.band_v0,
                       a.view_base + it);
         } else {
           mbar_arrive(&full[s]);
@@ -186,15 +230,15 @@ __global__ void __launch_bounds__(NTHREADS, 2)
   // ---------------- consumers: one (x, y) column, K voxels each -------------
   const int w = tid >> 5, lane = tid & 31;
   const int lx = lane & 15, ly = 2 * w + (lane >> 4);
-  const int gx = blockIdx.x * BX + lx, gy = blockIdx.y * BY + ly;
-  const int zt0 = blockIdx.z * K;
+  const int gx = tile.x0 + lx, gy = tile.y0 + ly;
   const bool valid = gx < a.nx && gy < a.ny;
   const int ix = min(gx, a.nx - 1), iy = min(gy, a.ny - 1);
-  const float x = float(a.ox + double(ix) * a.sx);
-  const float y = float(a.oy + double(iy) * a.sy);
-  const float zf0 = float(a.oz + double(a.z0 + zt0) * a.sz);
-  const float dz = float(a.sz);
-  const int kmax = min(K, a.nz - zt0) - 1;  // clamp tail voxels into the tile
+  // offsets from the tile centre (exact small numbers)
+  const float dx = float((double(ix) - 0.5 * double(tile.x0 + tile.x1)) * a.sx);
+  const float dy = float((double(iy) - 0.5 * double(tile.y0 + tile.y1)) * a.sy);
+  const float dz0 = float((double(tile.z0) - 0.5 * double(tile.z0 + tile.z1)) * a.sz);
+  const float sz = float(a.sz);
+  const int kmax = tile.z1 - tile.z0;  // clamp tail voxels into the tile
   const uint32_t box_base = smem_u32(boxes);
   constexpr uint32_t ROWB = BOXU * 4;
   constexpr float MAGIC = 12582912.0f;  // 1.5 * 2^23: t = M + floor(v) under round-down
@@ -207,24 +251,23 @@ __global__ void __launch_bounds__(NTHREADS, 2)
   for (int it = 0; it < a.n_views; ++it) {
     const int s = it % STAGES;
     mbar_wait(&full[s], (it / STAGES) & 1);
-    const int4 h = hdr[s];
-    const float4 r0 = c_views[3 * it], r1 = c_views[3 * it + 1], r2 = c_views[3 * it + 2];
-    if (h.z == MODE_FAST) {
-      const uint32_t sbase = box_base + uint32_t(s * box_elems) * 4u;
+    const float4 U = hdr[s].U, V = hdr[s].V, W = hdr[s].W;
+    const int mode = hdr[s].meta.z;
+    const float un = fmaf(U.x, dx, fmaf(U.y, dy, U.w));
+    const float vn = fmaf(V.x, dx, fmaf(V.y, dy, V.w));
+    const float hz0 = fmaf(W.x, dx, fmaf(W.y, dy, W.w));
+    if (mode == MODE_FAST) {
+      const uint32_t sbase = box_base + uint32_t(s * stage_elems) * 4u;
       if (CIRC) {
         // P[0][2] == P[2][2] == 0: u and 1/w^2 are constant along z and v is
         // affine in z (SURVEY §7 hard part (b)).
-        const float hx = fmaf(r0.x, x, fmaf(r0.y, y, r0.w));
-        const float hy = fmaf(r1.x, x, fmaf(r1.y, y, r1.w));
-        const float hz = fmaf(r2.x, x, fmaf(r2.y, y, r2.w));
-        const float r = __frcp_rn(hz);
+        const float r = __frcp_rn(hz0);
         const float invw2 = a.sid2 * r * r;
-        const float u = fmaf(hx, r, -float(h.x));
+        const float u = un * r;
         const float fu = floorf(u);
         const float wu = u - fu;
-        const float p6r = r1.z * r;
-        const float v0 = fmaf(p6r, zf0, fmaf(hy, r, -float(h.y)));
-        const float dv = p6r * dz;
+        const float v0 = fmaf(V.z, dz0, vn) * r;
+        const float dv = V.z * sz * r;
         const uint32_t cbase = sbase + uint32_t(int(fu)) * 4u - MAGIC_BITS * ROWB;
 #pragma unroll
         for (int k = 0; k < K; ++k) {
@@ -240,16 +283,12 @@ __global__ void __launch_bounds__(NTHREADS, 2)
         }
       } else {
         // general calibrated matrices: full projective map per voxel
-        const float hx0 = fmaf(r0.x, x, fmaf(r0.y, y, r0.w));
-        const float hy0 = fmaf(r1.x, x, fmaf(r1.y, y, r1.w));
-        const float hz0 = fmaf(r2.x, x, fmaf(r2.y, y, r2.w));
 #pragma unroll
         for (int k = 0; k < K; ++k) {
-          const float z = fmaf(float(min(k, kmax)), dz, zf0);
-          const float hz = fmaf(r2.z, z, hz0);
-          const float r = __frcp_rn(hz);
-          const float u = fmaf(fmaf(r0.z, z, hx0), r, -float(h.x));
-          const float vk = fmaf(fmaf(r1.z, z, hy0), r, -float(h.y));
+          const float dz = fmaf(float(min(k, kmax)), sz, dz0);
+          const float r = __frcp_rn(fmaf(W.z, dz, hz0));
+          const float u = fmaf(U.z, dz, un) * r;
+          const float vk = fmaf(V.z, dz, vn) * r;
           const float tu = __fadd_rd(u, MAGIC);
           const float tv = __fadd_rd(vk, MAGIC);
           const float wu = u - (tu - MAGIC);
@@ -263,14 +302,16 @@ __global__ void __launch_bounds__(NTHREADS, 2)
           acc[k] = fmaf(fmaf(wv, bot - top, top), a.sid2 * r * r, acc[k]);
         }
       }
-    } else if (h.z == MODE_SLOW) {
+    } else if (mode == MODE_SLOW) {
+      // absolute frame (ub = vb = 0): per-voxel checks against the reference
       const float* img = a.sino + (long long)(a.view_base + it) * a.view_pitch;
 #pragma unroll
       for (int k = 0; k < K; ++k) {  // unrolled: acc[] must stay in registers
-        const float z = fmaf(float(min(k, kmax)), dz, zf0);
-        float u, v, hz;
-        project_point(r0, r1, r2, x, y, z, u, v, hz);
-        if (!(hz > 0.0f) || !(fabsf(u) < 4.0e6f) || !(fabsf(v) < 4.0e6f)) continue;
+        const float dz = fmaf(float(min(k, kmax)), sz, dz0);
+        const float hz = fmaf(W.z, dz, hz0);
+        if (!(hz > 0.0f)) continue;  // behind the source (projector.hpp:302)
+        const float u = fmaf(U.z, dz, un) / hz, v = fmaf(V.z, dz, vn) / hz;
+        if (!(fabsf(u) < 4.0e6f) || !(fabsf(v) < 4.0e6f)) continue;
         acc[k] += bilinear_global(a, img, u, v) * (a.sid2 / (hz * hz));
       }
     }
@@ -282,7 +323,7 @@ __global__ void __launch_bounds__(NTHREADS, 2)
 #pragma unroll
   for (int k = 0; k < K; ++k) {
     if (k > kmax) break;
-    float* o = a.vol + ((long long)(zt0 + k) * a.ny + iy) * a.nx + ix;
+    float* o = a.vol + ((long long)(tile.z0 + k) * a.ny + iy) * a.nx + ix;
     const float val = acc[k] * a.scale;
     *o = a.accumulate ? *o + val : val;
   }
@@ -379,9 +420,13 @@ __global__ void __launch_bounds__(256) cone_fp_kernel(const FpArgs a) {
   const long long nxp = a.nxp, nxyp = (long long)a.nxp * a.nyp;
   double total = 0.0;
   for (long long k0 = 0; k0 < n; k0 += 64) {
-    const float bx = float(p0x + double(k0) * ddx);
-    const float by = float(p0y + double(k0) * ddy);
-    const float bz = float(p0z + double(k0) * ddz);
+    // chunk anchor split into an integer cell and a small fp32 offset, so
+    // sample positions keep ~1e-5 voxel precision anywhere in a 1024^3 grid
+    const double ax = p0x + double(k0) * ddx, ay = p0y + double(k0) * ddy,
+                 az = p0z + double(k0) * ddz;
+    const double cx = floor(ax), cy = floor(ay), cz = floor(az);
+    const float bx = float(ax - cx), by = float(ay - cy), bz = float(az - cz);
+    const float* cell = a.vpad + (long long)cz * nxyp + (long long)cy * nxp + (long long)cx;
     const int m = int(min(64LL, n - k0));
     float sum = 0.0f;
     for (int j = 0; j < m; ++j) {
@@ -390,7 +435,7 @@ __global__ void __launch_bounds__(256) cone_fp_kernel(const FpArgs a) {
       const float pz = fmaf(float(j), fdz, bz);
       const float fx = floorf(px), fy = floorf(py), fz = floorf(pz);
       const float wx = px - fx, wy = py - fy, wz = pz - fz;
-      const float* b = a.vpad + (long long)int(fz) * nxyp + (long long)int(fy) * nxp + int(fx);
+      const float* b = cell + (long long)int(fz) * nxyp + (long long)int(fy) * nxp + int(fx);
       const float c00 = lerpf(__ldg(b), __ldg(b + 1), wx);
       const float c01 = lerpf(__ldg(b + nxp), __ldg(b + nxp + 1), wx);
       const float c10 = lerpf(__ldg(b + nxyp), __ldg(b + nxyp + 1), wx);
@@ -437,7 +482,7 @@ struct tg_cone_plan {
   double range = 0, sid = 0, sdd = 0;
   std::vector<double> mats, sources, invs, angles;
   bool circular = true;
-  float4* d_coef = nullptr;   // 3 x n_proj fp32 matrix rows
+  double* d_mats = nullptr;   // 12 x n_proj FP64 matrices (K1's constant bank source)
   double* d_geo = nullptr;    // 12 x n_proj: source + inverse block (FP64)
   int boxV = 0, boxU = 0;     // K1 TMA box
   int need_w = 0, need_h = 0;
@@ -514,7 +559,7 @@ void size_box(tg_cone_plan& p) {
   const long long total = (long long)tx * ty * tz * a.n_views;
   const int threads = 256;
   const long long blocks = (total + threads - 1) / threads;
-  footprint_kernel<<<unsigned(blocks), threads>>>(a, kK, tx, ty, tz, p.d_coef, d_need);
+  footprint_kernel<<<unsigned(blocks), threads>>>(a, kK, tx, ty, tz, p.d_mats, d_need);
   TG_LAUNCHED(1);
   int need[2] = {0, 0};
   TG_CUDA(cudaMemcpy(need, d_need, sizeof need, cudaMemcpyDeviceToHost));
@@ -572,8 +617,8 @@ void backproject_impl(tg_cone_plan& p, uint64_t z0, uint64_t nz, uint64_t v0, ui
   a.row_pitch = (long long)pitch;
   a.view_pitch = (long long)(pitch * n_rows);
   a.vol = d_slab;
-  const size_t smem = size_t(STAGES) * p.boxU * p.boxV * 4 + STAGES * sizeof(int4) +
-                      2 * STAGES * sizeof(uint64_t);
+  const size_t stage_elems = (size_t(p.boxU) * p.boxV + 31) & ~size_t(31);
+  const size_t smem = size_t(STAGES) * stage_elems * 4 + STAGES * 64 + 2 * STAGES * sizeof(uint64_t);
   KernelTimer timer;
   timer.start(st);
   for (uint64_t c0 = view0; c0 < view0 + n_views; c0 += kMaxConstViews) {
@@ -584,8 +629,8 @@ void backproject_impl(tg_cone_plan& p, uint64_t z0, uint64_t nz, uint64_t v0, ui
     a.accumulate = (c0 == view0) ? accumulate : 1;
     std::lock_guard<std::mutex> lk(g_bank.mu);
     // bank content key: (plan, first view, view count)
-    g_bank.acquire(p.device, (p.id << 40) ^ (c0 << 20) ^ cn, st, c_views, p.d_coef + 3 * c0,
-                   cn * 3 * sizeof(float4));
+    g_bank.acquire(p.device, (p.id << 40) ^ (c0 << 20) ^ cn, st, c_views, p.d_mats + 12 * c0,
+                   cn * 12 * sizeof(double));
     if (p.circular) launch_bp_u<true>(p.boxU, map, a, smem, st);
     else launch_bp_u<false>(p.boxU, map, a, smem, st);
     TG_LAUNCHED(1);
@@ -814,20 +859,16 @@ tg_status tg_cone_plan_create(const tg_cone_geometry* g, int device, tg_cone_pla
     p->sources.assign(g->sources, g->sources + 3 * n);
     p->invs.assign(g->inv_blocks, g->inv_blocks + 9 * n);
     p->angles.assign(g->angles, g->angles + n);
-    std::vector<float4> coef(3 * n);
     std::vector<double> geo(12 * n);
     for (uint64_t i = 0; i < n; ++i) {
       const double* m = g->matrices + 12 * i;
       if (m[2] != 0.0 || m[10] != 0.0) p->circular = false;
-      for (int r = 0; r < 3; ++r)
-        coef[3 * i + r] = make_float4(float(m[4 * r]), float(m[4 * r + 1]), float(m[4 * r + 2]),
-                                      float(m[4 * r + 3]));
       for (int k = 0; k < 3; ++k) geo[12 * i + k] = g->sources[3 * i + k];
       for (int k = 0; k < 9; ++k) geo[12 * i + 3 + k] = g->inv_blocks[9 * i + k];
     }
     DeviceGuard dg(device);
-    TG_CUDA(cudaMalloc(&p->d_coef, coef.size() * sizeof(float4)));
-    TG_CUDA(cudaMemcpy(p->d_coef, coef.data(), coef.size() * sizeof(float4), cudaMemcpyHostToDevice));
+    TG_CUDA(cudaMalloc(&p->d_mats, 12 * n * sizeof(double)));
+    TG_CUDA(cudaMemcpy(p->d_mats, g->matrices, 12 * n * sizeof(double), cudaMemcpyHostToDevice));
     TG_CUDA(cudaMalloc(&p->d_geo, geo.size() * sizeof(double)));
     TG_CUDA(cudaMemcpy(p->d_geo, geo.data(), geo.size() * sizeof(double), cudaMemcpyHostToDevice));
     size_box(*p);
@@ -840,7 +881,7 @@ tg_status tg_cone_plan_destroy(tg_cone_plan* p) {
     if (!p) return;
     g_bank.forget(p->id);
     DeviceGuard dg(p->device);
-    cudaFree(p->d_coef);
+    cudaFree(p->d_mats);
     cudaFree(p->d_geo);
     cudaFree(p->d_cos);
     cudaFree(p->d_parker);

@@ -23,7 +23,7 @@ constexpr int BX = 16, BY = 16;
 constexpr int NCONS = BX * BY;          // consumer threads (8 warps)
 constexpr int NTHREADS = NCONS + 32;    // + one producer warp
 constexpr int STAGES = 4;               // projection boxes in flight
-constexpr int kMaxConstViews = 1024;    // views per constant-bank upload
+constexpr int kMaxConstViews = 640;     // FP64 matrices per constant-bank upload (60 KB)
 constexpr int MODE_FAST = 0, MODE_SLOW = 1, MODE_SKIP = 2;
 
 struct BpArgs {
@@ -52,16 +52,6 @@ struct Footprint {
   bool ok;   // every corner in front of the source and finite
   bool hit;  // overlaps the detector at all
 };
-
-__device__ __forceinline__ void project_point(const float4& r0, const float4& r1, const float4& r2,
-                                              float x, float y, float z, float& u, float& v,
-                                              float& hz) {
-  const float hx = fmaf(r0.x, x, fmaf(r0.y, y, fmaf(r0.z, z, r0.w)));
-  const float hy = fmaf(r1.x, x, fmaf(r1.y, y, fmaf(r1.z, z, r1.w)));
-  hz = fmaf(r2.x, x, fmaf(r2.y, y, fmaf(r2.z, z, r2.w)));
-  u = hx / hz;
-  v = hy / hz;
-}
 
 }  // namespace cone
 }  // namespace tgb

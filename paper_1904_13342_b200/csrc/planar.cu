@@ -13,9 +13,9 @@
 namespace tgb {
 namespace planar {
 
-constexpr int kMaxConstViews = 4096;
-// per view: parallel (axis.x, axis.y, -, -); fan (r.x, r.y, sid*r.x, sid*r.y)
-__constant__ float4 c_pviews[kMaxConstViews];
+constexpr int kMaxConstViews = 2048;
+// per view (FP64): parallel -> detector axis (-r.y, r.x); fan -> ray r
+__constant__ double2 c_pviews[kMaxConstViews];
 static ConstBank g_bank;
 
 #define DADD __dadd_rn
@@ -105,14 +105,18 @@ __global__ void __launch_bounds__(256) planar_fp_kernel(const FpArgs a) {
   const float fdx = float(ddx), fdy = float(ddy);
   double total = 0.0;
   for (long long k0 = 0; k0 < n; k0 += 64) {
-    const float bx = float(p0x + double(k0) * ddx), by = float(p0y + double(k0) * ddy);
+    // integer cell + small fp32 offset keeps sample positions precise
+    const double ax = p0x + double(k0) * ddx, ay = p0y + double(k0) * ddy;
+    const double cx = floor(ax), cy = floor(ay);
+    const float bx = float(ax - cx), by = float(ay - cy);
+    const float* cell = a.ipad + (long long)cy * a.nxp + (long long)cx;
     const int m = int(min(64LL, n - k0));
     float sum = 0.0f;
     for (int k = 0; k < m; ++k) {
       const float px = fmaf(float(k), fdx, bx), py = fmaf(float(k), fdy, by);
       const float fx = floorf(px), fy = floorf(py);
       const float wx = px - fx, wy = py - fy;
-      const float* b = a.ipad + (long long)int(fy) * a.nxp + int(fx);
+      const float* b = cell + (long long)int(fy) * a.nxp + int(fx);
       sum += lerpf(lerpf(__ldg(b), __ldg(b + 1), wx), lerpf(__ldg(b + a.nxp), __ldg(b + a.nxp + 1), wx),
                    wy);
     }
@@ -124,8 +128,8 @@ __global__ void __launch_bounds__(256) planar_fp_kernel(const FpArgs a) {
 struct BpArgs {
   int nx, ny, nb, n_views, view_base;
   double ox, oy, sx, sy;
-  float det_origin, inv_ds;
-  float sid, sdd;
+  double det_origin, inv_ds;
+  double sid, sdd;
   int fan;
   float scale;
   int accumulate;
@@ -134,39 +138,42 @@ struct BpArgs {
 };
 
 // zero-padded linear interpolation along one sinogram row (projector.hpp:32-41)
-__device__ __forceinline__ float interp_row(const float* __restrict__ row, int n, float t) {
-  const float f = floorf(t);
+__device__ __forceinline__ double interp_row(const float* __restrict__ row, int n, double t) {
+  const double f = floor(t);
   const int i0 = int(f);
-  const float w1 = t - f;
-  const float a = (i0 >= 0 && i0 < n) ? __ldg(row + i0) : 0.0f;
-  const float b = (i0 + 1 >= 0 && i0 + 1 < n) ? __ldg(row + i0 + 1) : 0.0f;
-  return fmaf(w1, b - a, a);
+  const double w1 = t - f;
+  double acc = 0.0;
+  if (i0 >= 0 && i0 < n) acc += (1.0 - w1) * double(__ldg(row + i0));
+  if (i0 + 1 >= 0 && i0 + 1 < n) acc += w1 * double(__ldg(row + i0 + 1));
+  return acc;
 }
 
+// K6 / K4: one thread per pixel, views from the constant bank.  These 2D
+// operators are launch-bound at the BASELINE sizes (c1 2.4e7, c2 9.4e7
+// updates), so the per-update geometry runs in FP64 like the reference.
 __global__ void __launch_bounds__(256) planar_bp_kernel(const BpArgs a) {
   const int ix = blockIdx.x * 32 + threadIdx.x, iy = blockIdx.y * 8 + threadIdx.y;
   if (ix >= a.nx || iy >= a.ny) return;
-  const float x = float(a.ox + double(ix) * a.sx);
-  const float y = float(a.oy + double(iy) * a.sy);
-  float acc = 0.0f;
+  const double x = a.ox + double(ix) * a.sx;
+  const double y = a.oy + double(iy) * a.sy;
+  double acc = 0.0;
   for (int i = 0; i < a.n_views; ++i) {
-    const float4 c = c_pviews[i];
+    const double2 c = c_pviews[i];
     const float* row = a.sino + (long long)(a.view_base + i) * a.nb;
     if (!a.fan) {
-      const float s = fmaf(x, c.x, y * c.y);
+      const double s = x * c.x + y * c.y;
       acc += interp_row(row, a.nb, (s - a.det_origin) * a.inv_ds);
     } else {
-      const float qx = x + c.z, qy = y + c.w;
-      const float depth = fmaf(qx, c.x, qy * c.y);
-      if (!(depth > 0.0f)) continue;  // behind the source
-      // detector axis (-r.y, r.x)
-      const float u = a.sdd * fmaf(qy, c.x, -qx * c.y) / depth;
-      const float U = depth / a.sid;
+      const double qx = x + a.sid * c.x, qy = y + a.sid * c.y;
+      const double depth = qx * c.x + qy * c.y;
+      if (depth <= 0.0) continue;  // behind the source
+      const double u = a.sdd * (qx * -c.y + qy * c.x) / depth;
+      const double U = depth / a.sid;
       acc += interp_row(row, a.nb, (u - a.det_origin) * a.inv_ds) / (U * U);
     }
   }
   float* o = a.img + (long long)iy * a.nx + ix;
-  const float v = acc * a.scale;
+  const float v = float(acc) * a.scale;
   *o = a.accumulate ? *o + v : v;
 }
 
@@ -195,7 +202,7 @@ struct tg_planar_plan {
   double range = 0, sid = 0, sdd = 0;
   bool fan = false;
   double* d_rays = nullptr;
-  float4* d_coef = nullptr;
+  double2* d_coef = nullptr;
   float* d_ipad = nullptr;
   std::mutex mu;
 };
@@ -247,10 +254,10 @@ void planar_backproject_impl(tg_planar_plan& p, const float* d_sino, float* d_im
   a.oy = p.vol.origin[1];
   a.sx = p.vol.spacing[0];
   a.sy = p.vol.spacing[1];
-  a.det_origin = float(p.det.origin);
-  a.inv_ds = float(1.0 / p.det.spacing);
-  a.sid = float(p.sid);
-  a.sdd = float(p.sdd);
+  a.det_origin = p.det.origin;
+  a.inv_ds = 1.0 / p.det.spacing;
+  a.sid = p.sid;
+  a.sdd = p.sdd;
   a.fan = p.fan;
   a.sino = d_sino;
   a.img = d_img;
@@ -264,7 +271,7 @@ void planar_backproject_impl(tg_planar_plan& p, const float* d_sino, float* d_im
     a.scale = scale;
     a.accumulate = c0 == 0 ? accumulate : 1;
     std::lock_guard<std::mutex> lk(g_bank.mu);
-    g_bank.acquire(p.device, (p.id << 24) ^ c0, st, c_pviews, p.d_coef + c0, cn * sizeof(float4));
+    g_bank.acquire(p.device, (p.id << 24) ^ c0, st, c_pviews, p.d_coef + c0, cn * sizeof(double2));
     planar_bp_kernel<<<grid, dim3(32, 8), 0, st>>>(a);
     TG_LAUNCHED(1);
     g_bank.release(p.device, st);
@@ -302,17 +309,16 @@ tg_status tg_planar_plan_create(const tg_planar_geometry* g, int device, tg_plan
     p->sdd = g->sdd;
     p->fan = fan;
     const uint64_t n = g->n_projections;
-    std::vector<float4> coef(n);
+    std::vector<double2> coef(n);
     for (uint64_t i = 0; i < n; ++i) {
       const double rx = g->rays[2 * i], ry = g->rays[2 * i + 1];
-      coef[i] = fan ? make_float4(float(rx), float(ry), float(g->sid * rx), float(g->sid * ry))
-                    : make_float4(float(-ry), float(rx), 0.f, 0.f);
+      coef[i] = fan ? make_double2(rx, ry) : make_double2(-ry, rx);
     }
     DeviceGuard dg(device);
     TG_CUDA(cudaMalloc(&p->d_rays, 2 * n * sizeof(double)));
     TG_CUDA(cudaMemcpy(p->d_rays, g->rays, 2 * n * sizeof(double), cudaMemcpyHostToDevice));
-    TG_CUDA(cudaMalloc(&p->d_coef, n * sizeof(float4)));
-    TG_CUDA(cudaMemcpy(p->d_coef, coef.data(), n * sizeof(float4), cudaMemcpyHostToDevice));
+    TG_CUDA(cudaMalloc(&p->d_coef, n * sizeof(double2)));
+    TG_CUDA(cudaMemcpy(p->d_coef, coef.data(), n * sizeof(double2), cudaMemcpyHostToDevice));
     *out = p.release();
   });
 }
