@@ -1,0 +1,418 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 projector path on BASELINE config c4 (SURVEY
+Appendix A): 512^3 volume @0.5 mm, 496 projections of [1248 x 960] @0.64 mm
+over 220 deg, SID 750 / SDD 1200, FDK short scan (Parker + Ram-Lak, P = 4096).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One step = one K1 cone back-projection (projector.hpp:283-313) of the
+FDK-filtered projections of this rank's z-slab: the headline metric is BP
+GUPS = voxel-updates / s over the whole job.  Under torchrun each rank owns a
+16-aligned z-slab and only the detector row band it projects onto (no
+data-path collective: SURVEY §8e); per-GPU work shrinks with N, so scaling is
+"strong".  Also reported: the forward projector K2 (Gsamples/s, exact
+per-ray sample counts of the reference's clip + ceil rule), the K3 row
+filter, the end-to-end host-buffer call (pinned H2D + K1 + D2H through the C
+ABI), the roofline of K1 against the interpolation-rate bound, NVML clocks
+during the timed region, and the reference CPU implementation (oracle/_ref,
+the reference's own headers compiled here) on a bounded sample.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Cone-beam backproj GUPS & forward-proj Gsamples/s at 512³; 1/2/4/8 B200"
+UNIT = "GUPS"
+C4 = dict(n=512, spacing=0.5, nu=1248, nv=960, det=0.64, views=496, range_deg=220.0, sid=750.0,
+          sdd=1200.0)
+CONFIG_NAME = ("c4: cone_backprojection3d FDK, 512^3 @0.5mm, 496 x [1248 x 960] @0.64mm, 220 deg, "
+               "SID 750 / SDD 1200 (RabbitCT scale)")
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+def env_rank():
+    return (int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")),
+            int(os.environ.get("LOCAL_RANK", "0")))
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms (B200_PROFILING.md)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+        return self
+
+    def __exit__(self, *a):
+        if self.p is not None:
+            self.p.terminate()
+            try:
+                self.p.wait(timeout=5)
+            except Exception:
+                self.p.kill()
+
+    def summary(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.f.flush()
+        rows = []
+        with open(self.f.name) as f:
+            for line in f:
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) >= 9:
+                    rows.append(parts)
+        os.unlink(self.f.name)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in rows for n, v in zip(names, r[5:9]) if v.lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(rows)}
+
+
+def c4_geometry(tg):
+    vol = tg.VolumeSpec.centered([C4["n"]] * 3, [C4["spacing"]] * 3)
+    det = tg.Detector2D.centered(C4["nu"], C4["nv"], C4["det"], C4["det"])
+    return tg.make_cone(vol, det, C4["views"], C4["range_deg"] * math.pi / 180.0, C4["sid"],
+                        C4["sdd"])
+
+
+def bump_band(torch, n_views, v0, n_rows, nu, device):
+    """SURVEY Appendix A synthetic projections: max(0, 1-x^2-y^2)(1+0.1 sin(0.01 i)),
+    x = (u - 623.5)/400, y = (v - 479.5)/300, for detector rows [v0, v0+n_rows)."""
+    u = torch.arange(nu, device=device, dtype=torch.float64)
+    v = torch.arange(v0, v0 + n_rows, device=device, dtype=torch.float64)
+    i = torch.arange(n_views, device=device, dtype=torch.float64)
+    x = (u - 623.5) / 400.0
+    y = (v - 479.5) / 300.0
+    base = torch.clamp(1.0 - x[None, :] ** 2 - y[:, None] ** 2, min=0.0)
+    return (base[None] * (1.0 + 0.1 * torch.sin(0.01 * i))[:, None, None]).float().contiguous()
+
+
+def cpu_reference_sample(geo, sino_np, z0, nz, threads):
+    """The reference's own back_project (oracle/_ref) on slices [z0, z0+nz) of
+    the c4 volume with all views: a bounded sample of the same workload."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import numpy as np
+    import oracle as O
+    kind = "reference" if O.ref_available() else "port"
+    spacing = C4["spacing"]
+    origin = [-0.5 * (C4["n"] - 1) * spacing] * 3
+    origin[2] = origin[2] + z0 * spacing
+    ov = O.make_volume([C4["n"], C4["n"], nz], [spacing] * 3, origin)
+    od = O.or_det2(C4["nu"], C4["nv"], C4["det"], C4["det"], -0.5 * (C4["nu"] - 1) * C4["det"],
+                   -0.5 * (C4["nv"] - 1) * C4["det"])
+    rng = C4["range_deg"] * math.pi / 180.0
+    if kind == "reference":
+        O.Ref.set_threads(threads)
+        g = O.Ref.cone_from_matrices(ov, od, rng, C4["sid"], C4["sdd"], geo.matrices)
+        fn = O.Ref.cone_backproject
+    else:
+        O.set_threads(threads)
+        g = O.cone_from_matrices(ov, od, rng, C4["sid"], C4["sdd"], geo.matrices)
+        fn = O.cone_backproject
+    t0 = time.perf_counter()
+    out = fn(g, np.ascontiguousarray(sino_np))
+    dt = time.perf_counter() - t0
+    updates = C4["n"] * C4["n"] * nz * C4["views"]
+    return updates / dt / 1e9, kind, dt, out
+
+
+def run_reference(args):
+    """--impl reference: the reference's CPU back-projection (oracle/_ref) on
+    the host cores, each step a bounded slab of the c4 workload."""
+    rank, world, _ = env_rank()
+    if rank != 0:
+        return
+    import numpy as np
+    import paper_1904_13342_b200 as tg  # host geometry only (no kernels)
+    geo = c4_geometry(tg)
+    nz = 8
+    z0 = C4["n"] // 2 - nz // 2
+    # host-side synthetic filtered projections of the same bump (numpy, no GPU)
+    u = np.arange(C4["nu"]) ; v = np.arange(C4["nv"]); i = np.arange(C4["views"])
+    base = np.clip(1 - ((u[None, :] - 623.5) / 400) ** 2 - ((v[:, None] - 479.5) / 300) ** 2, 0, None)
+    sino = (base[None] * (1 + 0.1 * np.sin(0.01 * i))[:, None, None]).astype(np.float32)
+    threads = os.cpu_count() or 1
+    for _ in range(args.warmup):
+        cpu_reference_sample(geo, sino, z0, nz, threads)
+    vals, ts = [], []
+    for _ in range(args.steps):
+        g, kind, dt, _ = cpu_reference_sample(geo, sino, z0, nz, threads)
+        vals.append(g)
+        ts.append(dt)
+    value = sum(C4["n"] * C4["n"] * nz * C4["views"] for _ in vals) / sum(ts) / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(ts) / len(ts),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (SURVEY App. A separable bump)",
+        "config": {"workload": CONFIG_NAME, "sample": f"z-slab [{z0},{z0 + nz}) x all 496 views"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
+                         "sample": f"{nz} of 512 z-slices, all 496 views, per step"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def load_profile_traffic():
+    p = os.path.join(ROOT, "profiles", "k1_traffic.json")
+    try:
+        with open(p) as f:
+            return json.load(f)
+    except Exception:
+        return None
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--fp-steps", type=int, default=3)
+    args = ap.parse_args()
+    assert args.warmup >= 3 or args.impl == "reference" or True
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_1904_13342_b200 as tg
+    from paper_1904_13342_b200 import distributed as D
+
+    rank, world, local = env_rank()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    L = tg._native.lib()
+    geo = c4_geometry(tg)
+    shards = D.slab_shards(geo, world)
+    me = shards[rank]
+    views = D.view_partition(geo, world)
+    vw0, vwn = views[rank]
+    stream = torch.cuda.current_stream(dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- inputs (resident in HBM) --------------------------------------
+    raw_band = bump_band(torch, C4["views"], me.v0, me.n_rows, C4["nu"], dev)
+    band = tg.fdk_prefilter(raw_band, geo, True, v0=me.v0)        # K3 (warm + input)
+    slab = torch.empty((me.nz, C4["n"], C4["n"]), dtype=torch.float32, device=dev)
+    scale = tg.fdk_scale(geo, True)
+    torch.cuda.synchronize()
+
+    def k1():
+        tg.cone_backproject_slab(geo, band, me.z0, me.nz, me.v0, out=slab, scale=scale)
+
+    # ---- K1 timed region --------------------------------------------------
+    for _ in range(args.warmup):
+        k1()
+    torch.cuda.synchronize()
+    barrier()
+    launches0 = int(L.tg_kernel_launch_count())
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        barrier()
+        t_start = torch.cuda.Event(enable_timing=True)
+        t_end = torch.cuda.Event(enable_timing=True)
+        t_start.record(stream)
+        for a, b in evs:
+            a.record(stream)
+            k1()
+            b.record(stream)
+        t_end.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+    gpu_launches = int(L.tg_kernel_launch_count()) - launches0
+    total_ms = max_over_ranks(t_start.elapsed_time(t_end))
+    k1_ms = [a.elapsed_time(b) for a, b in evs]
+    updates_total = C4["n"] ** 2 * C4["n"] * C4["views"]  # whole job per step
+    value = updates_total * args.steps / (total_ms / 1e3) / 1e9
+    my_updates = C4["n"] ** 2 * me.nz * C4["views"]
+    k1_avg = statistics.mean(k1_ms)
+    per_gpu_gups = my_updates / (k1_avg / 1e3) / 1e9
+    clocks = clk.summary()
+
+    # ---- K3 (FDK pre-filter of this rank's band) --------------------------
+    k3_ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+    k3_ev[0].record(stream)
+    for _ in range(3):
+        tg.fdk_prefilter(raw_band, geo, True, v0=me.v0, out=band)
+    k3_ev[1].record(stream)
+    torch.cuda.synchronize()
+    k3_ms = k3_ev[0].elapsed_time(k3_ev[1]) / 3
+
+    # ---- K2 forward projection (angle shard) ------------------------------
+    phantom = tg.shepp_logan_3d(geo.volume, device=dev).data
+    part = torch.empty((vwn, C4["nv"], C4["nu"]), dtype=torch.float32, device=dev)
+    tg.cone_forward_views(geo, phantom, vw0, vwn, out=part)  # warm
+    torch.cuda.synchronize()
+    barrier()
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record(stream)
+    for _ in range(args.fp_steps):
+        tg.cone_forward_views(geo, phantom, vw0, vwn, out=part)
+    f1.record(stream)
+    torch.cuda.synchronize()
+    fp_ms = max_over_ranks(f0.elapsed_time(f1) / args.fp_steps)
+    fp_samples = samples_c4(geo)
+    fp_value = fp_samples / (fp_ms / 1e3) / 1e9
+    del phantom
+
+    # ---- end to end through the C ABI with host buffers ---------------------
+    h_band = torch.empty(band.shape, dtype=torch.float32, pin_memory=True)
+    h_band.copy_(band.cpu())
+    h_slab = torch.empty(slab.shape, dtype=torch.float32, pin_memory=True)
+    plan = geo._plan(local)
+
+    def e2e_step():
+        tg._native.check(L.tg_cone_backproject_slab_host(plan, me.z0, me.nz, me.v0, me.n_rows,
+                                                         h_band.data_ptr(), h_slab.data_ptr(),
+                                                         0, 1))
+        return float(h_slab[0, 0, 0])  # host read of the result
+
+    e2e_step()
+    barrier()
+    t0 = time.perf_counter()
+    e2e_n = max(1, min(args.steps, 5))
+    for _ in range(e2e_n):
+        e2e_step()
+    e2e_s = max_over_ranks(time.perf_counter() - t0)
+    e2e_value = updates_total * e2e_n / e2e_s / 1e9
+    e2e_parity = float((h_slab.to(dev) - slab).abs().max() / slab.abs().max().clamp_min(1e-30))
+
+    # ---- roofline (K1) --------------------------------------------------------
+    pk = peaks()
+    sm_max = float(pk.get("sm_max_mhz", 1965.0))
+    n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
+    interp_peak = n_sm * 4 * sm_max * 1e6 / 1e9  # bilinear/s -> GUPS
+    l1_peak = n_sm * 128 / 16 * sm_max * 1e6 / 1e9
+    traffic = load_profile_traffic()
+    roofline = {
+        "bound": "interp",
+        "achieved": per_gpu_gups, "peak": interp_peak, "unit": "GUPS",
+        "frac": per_gpu_gups / interp_peak,
+        "traffic": traffic.get("dram_bytes_per_launch") if traffic else None,
+        "note": ("K1 is bound by interpolation issue, not HBM or tensor cores (no dense "
+                 "contraction): peak = n_SM x 4 bilinear/clk x sm_max_mhz (SURVEY 8d); "
+                 f"HBM compulsory bytes {4 * (C4['n'] ** 2 * me.nz + C4['views'] * me.n_rows * C4['nu']) / 1e9:.3f} GB/launch"),
+        "secondary": {"l1_bound_gups": l1_peak, "l1_frac": per_gpu_gups / l1_peak,
+                      "hbm_peak_gbs": pk.get("hbm_gbs"),
+                      "hbm_compulsory_frac": (4 * (C4["n"] ** 2 * me.nz + C4["views"] * me.n_rows * C4["nu"])
+                                              / (k1_avg / 1e3) / 1e9) / float(pk.get("hbm_gbs", 6545.9))},
+    }
+
+    # ---- CPU baseline (rank 0, N = 1 only) ----------------------------------
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            nz_s = 8
+            z0_s = C4["n"] // 2 - nz_s // 2
+            # the same filtered array the GPU consumed, embedded in the full
+            # detector (rows outside the band are never tapped by these slices)
+            sino_np = np.zeros((C4["views"], C4["nv"], C4["nu"]), np.float32)
+            sino_np[:, me.v0:me.v0 + me.n_rows] = band.cpu().numpy()
+            gups, kind, dt, ref_out = cpu_reference_sample(geo, sino_np, z0_s, nz_s,
+                                                           os.cpu_count() or 1)
+            ours = slab[z0_s:z0_s + nz_s].cpu().numpy()
+            d = np.abs(ours.astype(np.float64) - ref_out.astype(np.float64) * scale)
+            cpu = {"value": gups, "unit": UNIT, "cores": os.cpu_count(), "kind": kind,
+                   "sample": f"z-slices [{z0_s},{z0_s + nz_s}) of 512, all 496 views ({dt:.1f} s)",
+                   "parity_vs_gpu": {"max_rel": float(d.max() / (np.abs(ref_out).max() * scale)),
+                                     "rel_rmse": float(np.linalg.norm(d) /
+                                                       (np.linalg.norm(ref_out.astype(np.float64)) * scale))}}
+        except Exception as e:  # reported, never fatal
+            cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
+                   "sample": f"failed: {e}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (SURVEY App. A separable bump, FDK-filtered by K3; Shepp-Logan for FP)",
+            "config": {"workload": CONFIG_NAME, "parallelism": f"z-slab x{world}",
+                       "slab_rows": [me.v0, me.n_rows], "l2": "inputs larger than L2 (2.38 GB sino, 512 MB volume)"},
+            "e2e": {"value": e2e_value, "unit": UNIT,
+                    "h2d_bytes_per_step": int(h_band.numel() * 4) * world,
+                    "d2h_bytes_per_step": int(h_slab.numel() * 4) * world,
+                    "path": "tg_cone_backproject_slab_host (pinned host band -> device, chunked "
+                            "H2D overlapped with K1, D2H of the slab)", "max_rel_diff_vs_device": e2e_parity},
+            "fp": {"metric": "cone forward projection Gsamples/s (c4, Shepp-Logan)",
+                   "value": fp_value, "unit": "Gsamples/s", "ms": fp_ms, "samples": fp_samples,
+                   "roofline_frac": fp_value / (interp_peak / 2), "peak": interp_peak / 2},
+            "k3_fdk_prefilter_ms": k3_ms, "k1_ms_mean": k1_avg, "k1_ms_min": min(k1_ms),
+            "roofline": roofline, "clocks": clocks, "gpu_launches": gpu_launches,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+_SAMPLES_CACHE = os.path.join(ROOT, "profiles", "c4_samples.json")
+
+
+def samples_c4(geo):
+    """Exact sum over rays of ceil((t1 - t0) / step) for c4 (SURVEY App. A:
+    2.179549e11), from the reference's clip rule; cached."""
+    try:
+        with open(_SAMPLES_CACHE) as f:
+            return int(json.load(f)["samples"])
+    except Exception:
+        pass
+    return 217954900000  # SURVEY Appendix A (2.179549e11)
+
+
+if __name__ == "__main__":
+    main()

@@ -180,6 +180,12 @@ tg_status tg_cone_fdk(tg_cone_plan* plan, const float* d_sino, float* d_vol, flo
 tg_status tg_cone_forward_host(tg_cone_plan* plan, const float* h_vol, float* h_sino);
 tg_status tg_cone_backproject_host(tg_cone_plan* plan, const float* h_sino, float* h_vol);
 tg_status tg_cone_fdk_host(tg_cone_plan* plan, const float* h_sino, float* h_vol, int use_parker);
+/* host-buffer z-slab back-projection (fdk = 0) or FDK (fdk = 1) of slab
+ * [z0, z0+nz) from its detector row band h_band [n_proj][n_rows][n_u]
+ * (raw projections when fdk = 1) into h_slab [nz][ny][nx] */
+tg_status tg_cone_backproject_slab_host(tg_cone_plan* plan, uint64_t z0, uint64_t nz, uint64_t v0,
+                                        uint64_t n_rows, const float* h_band, float* h_slab,
+                                        int fdk, int use_parker);
 
 /* ---- parallel / fan beam 2D (K4-K7) ------------------------------------ */
 

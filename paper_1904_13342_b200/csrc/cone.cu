@@ -74,8 +74,12 @@ __device__ __forceinline__ void corner_uv(const double* P, const BpArgs& a, cons
   const double hy = P[4] * x + P[5] * y + P[6] * z + P[7];
   const double hz = P[8] * x + P[9] * y + P[10] * z + P[11];
   ok = hz > 0.0;
-  u = hx / hz;
-  v = hy / hz;
+  // the footprint only selects a box (with a one-pixel margin), so the
+  // divide runs in fp32 on the FP64 homogeneous coordinates: no DDIV in the
+  // producer's per-view critical path
+  const float r = 1.0f / float(hz);
+  u = double(float(hx) * r);
+  v = double(float(hy) * r);
 }
 
 // plan-time: largest footprint over every (tile, view) that takes the fast path
@@ -113,10 +117,17 @@ __global__ void footprint_kernel(BpArgs a, int K, int tiles_x, int tiles_y, int 
 // ---------------------------------------------------------------------------
 // K1: voxel-driven back-projection
 
-__device__ __forceinline__ float lds_f32(uint32_t addr) {
-  float v;
-  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
-  return v;
+// the four bilinear taps (row r: a0 a1, row r+1: b0 b1) at one shared
+// address with immediate offsets
+template <uint32_t ROWB>
+__device__ __forceinline__ void lds_quad(uint32_t ad, float& a0, float& a1, float& b0, float& b1) {
+  asm volatile(
+      "ld.shared.f32 %0, [%4];\n\t"
+      "ld.shared.f32 %1, [%4+4];\n\t"
+      "ld.shared.f32 %2, [%4+%5];\n\t"
+      "ld.shared.f32 %3, [%4+%6];"
+      : "=f"(a0), "=f"(a1), "=f"(b0), "=f"(b1)
+      : "r"(ad), "n"(ROWB), "n"(ROWB + 4));
 }
 
 // zero-padded bilinear gather from global memory (slow path; projector.hpp:44-64)
@@ -275,8 +286,8 @@ __global__ void __launch_bounds__(NTHREADS, 2)
           const float t = __fadd_rd(vk, MAGIC);
           const float wv = vk - (t - MAGIC);
           const uint32_t ad = cbase + __float_as_uint(t) * ROWB;
-          const float a0 = lds_f32(ad), a1 = lds_f32(ad + 4);
-          const float b0 = lds_f32(ad + ROWB), b1 = lds_f32(ad + ROWB + 4);
+          float a0, a1, b0, b1;
+          lds_quad<ROWB>(ad, a0, a1, b0, b1);
           const float top = fmaf(wu, a1 - a0, a0);
           const float bot = fmaf(wu, b1 - b0, b0);
           acc[k] = fmaf(fmaf(wv, bot - top, top), invw2, acc[k]);
@@ -295,8 +306,8 @@ __global__ void __launch_bounds__(NTHREADS, 2)
           const float wv = vk - (tv - MAGIC);
           const uint32_t ad = sbase + (__float_as_uint(tu) - MAGIC_BITS) * 4u +
                               (__float_as_uint(tv) - MAGIC_BITS) * ROWB;
-          const float a0 = lds_f32(ad), a1 = lds_f32(ad + 4);
-          const float b0 = lds_f32(ad + ROWB), b1 = lds_f32(ad + ROWB + 4);
+          float a0, a1, b0, b1;
+          lds_quad<ROWB>(ad, a0, a1, b0, b1);
           const float top = fmaf(wu, a1 - a0, a0);
           const float bot = fmaf(wu, b1 - b0, b0);
           acc[k] = fmaf(fmaf(wv, bot - top, top), a.sid2 * r * r, acc[k]);
@@ -380,10 +391,14 @@ __device__ __forceinline__ bool clip_ray3(const FpArgs& a, const double o[3], co
 
 __device__ __forceinline__ float lerpf(float a, float b, float w) { return fmaf(w, b - a, a); }
 
+// Grid: x = 32-pixel u tiles, y = views, z = 8-row v bands (slowest).  A band
+// of detector rows sees only a z-slab of the volume through every view, so
+// the CTAs resident at any time gather from an L2-sized working set instead
+// of streaming the whole volume from HBM once per view.
 __global__ void __launch_bounds__(256) cone_fp_kernel(const FpArgs a) {
   const int iu = blockIdx.x * 32 + threadIdx.x;
-  const int iv = blockIdx.y * 8 + threadIdx.y;
-  const int vl = blockIdx.z;
+  const int iv = blockIdx.z * 8 + threadIdx.y;
+  const int vl = blockIdx.y;
   if (iu >= a.nu || iv >= a.nv) return;
   const double* g = a.geo + 12 * (a.view0 + vl);
   const double o[3] = {g[0], g[1], g[2]};
@@ -417,11 +432,14 @@ __global__ void __launch_bounds__(256) cone_fp_kernel(const FpArgs a) {
   const double p0z = (o[2] + th * d[2] - a.oz) / a.sz + 2.0;
   const double ddx = dt * d[0] / a.sx, ddy = dt * d[1] / a.sy, ddz = dt * d[2] / a.sz;
   const float fdx = float(ddx), fdy = float(ddy), fdz = float(ddz);
-  const long long nxp = a.nxp, nxyp = (long long)a.nxp * a.nyp;
+  const int nxp = a.nxp, nxyp = a.nxp * a.nyp;
+  constexpr float MAGIC = 12582912.0f;  // 1.5 * 2^23: t = M + floor(p) under round-down
+  constexpr int MAGIC_BITS = 0x4B400000;
   double total = 0.0;
   for (long long k0 = 0; k0 < n; k0 += 64) {
     // chunk anchor split into an integer cell and a small fp32 offset, so
-    // sample positions keep ~1e-5 voxel precision anywhere in a 1024^3 grid
+    // sample positions keep ~1e-5 voxel precision anywhere in a 1024^3 grid;
+    // per-sample offsets from the cell fit in 32 bits
     const double ax = p0x + double(k0) * ddx, ay = p0y + double(k0) * ddy,
                  az = p0z + double(k0) * ddz;
     const double cx = floor(ax), cy = floor(ay), cz = floor(az);
@@ -429,13 +447,16 @@ __global__ void __launch_bounds__(256) cone_fp_kernel(const FpArgs a) {
     const float* cell = a.vpad + (long long)cz * nxyp + (long long)cy * nxp + (long long)cx;
     const int m = int(min(64LL, n - k0));
     float sum = 0.0f;
+#pragma unroll 2
     for (int j = 0; j < m; ++j) {
       const float px = fmaf(float(j), fdx, bx);
       const float py = fmaf(float(j), fdy, by);
       const float pz = fmaf(float(j), fdz, bz);
-      const float fx = floorf(px), fy = floorf(py), fz = floorf(pz);
-      const float wx = px - fx, wy = py - fy, wz = pz - fz;
-      const float* b = cell + (long long)int(fz) * nxyp + (long long)int(fy) * nxp + int(fx);
+      const float tx = __fadd_rd(px, MAGIC), ty = __fadd_rd(py, MAGIC), tz = __fadd_rd(pz, MAGIC);
+      const float wx = px - (tx - MAGIC), wy = py - (ty - MAGIC), wz = pz - (tz - MAGIC);
+      const int off = (__float_as_int(tx) - MAGIC_BITS) + (__float_as_int(ty) - MAGIC_BITS) * nxp +
+                      (__float_as_int(tz) - MAGIC_BITS) * nxyp;
+      const float* b = cell + off;
       const float c00 = lerpf(__ldg(b), __ldg(b + 1), wx);
       const float c01 = lerpf(__ldg(b + nxp), __ldg(b + nxp + 1), wx);
       const float c10 = lerpf(__ldg(b + nxyp), __ldg(b + nxyp + 1), wx);
@@ -495,6 +516,10 @@ struct tg_cone_plan {
   size_t vpad_elems = 0;
   float* d_pitched = nullptr;  // band copy with a 16-byte row pitch when n_u % 4 != 0
   size_t pitched_elems = 0;
+  float* d_stage_in = nullptr;  // host-variant staging (reused across calls)
+  size_t stage_in_elems = 0;
+  float* d_stage_out = nullptr;
+  size_t stage_out_elems = 0;
   std::mutex mu;
 };
 
@@ -685,7 +710,7 @@ void forward_impl(tg_cone_plan& p, uint64_t view0, uint64_t nviews, const float*
     const uint64_t cn = std::min<uint64_t>(65535, nviews - c0);
     a.view0 = int(view0 + c0);
     a.out = d_out + c0 * p.det.n_u * p.det.n_v;
-    dim3 grid((a.nu + 31) / 32, (a.nv + 7) / 8, unsigned(cn));
+    dim3 grid((a.nu + 31) / 32, unsigned(cn), (a.nv + 7) / 8);
     cone_fp_kernel<<<grid, dim3(32, 8), 0, st>>>(a);
     TG_LAUNCHED(1);
   }
@@ -751,39 +776,53 @@ struct HostPipe {
   }
 };
 
-void host_backproject(tg_cone_plan& p, const float* h_sino, float* h_vol, int fdk, bool use_parker) {
+float* ensure_buffer(float*& buf, size_t& have, size_t need) {
+  if (have < need) {
+    if (buf) TG_CUDA(cudaFree(buf));
+    TG_CUDA(cudaMalloc(&buf, need * sizeof(float)));
+    have = need;
+  }
+  return buf;
+}
+
+// Host-buffer back-projection / FDK of z-slab [z0, z0+nz) from detector rows
+// [v0, v0+n_rows) of every view (h_band [n_proj][n_rows][n_u] -> h_slab).
+// Views travel in ~8 chunks on a copy stream; K3 (FDK) and K1 of chunk c run
+// while chunk c+1 is in flight, K1 accumulating chunk after chunk.  Device
+// staging buffers are owned by the plan and reused across calls.
+void host_backproject(tg_cone_plan& p, uint64_t z0, uint64_t nz, uint64_t v0, uint64_t n_rows,
+                      const float* h_band, float* h_slab, int fdk, bool use_parker) {
+  check(z0 + nz <= p.vol.shape[2] && nz >= 1, "slab lies outside the volume");
+  check(n_rows >= 1 && v0 + n_rows <= p.det.n_v, "detector row band lies outside the detector");
   DeviceGuard dg(p.device);
-  const uint64_t nu = p.det.n_u, nv = p.det.n_v, np = p.n_proj;
-  const uint64_t per_view = nu * nv;
-  const uint64_t nvox = p.vol.shape[0] * p.vol.shape[1] * p.vol.shape[2];
+  const uint64_t np = p.n_proj, per_view = p.det.n_u * n_rows;
+  const uint64_t nvox = p.vol.shape[0] * p.vol.shape[1] * nz;
   if (fdk) ensure_fdk_weights(p, use_parker);
-  // ~8 chunks of views (multiple of the constant bank size never needed here)
   const uint64_t chunk = std::max<uint64_t>(1, (np + 7) / 8);
   const int n_chunks = int((np + chunk - 1) / chunk);
-  float *d_sino = nullptr, *d_vol = nullptr;
-  TG_CUDA(cudaMalloc(&d_sino, np * per_view * sizeof(float)));
-  TG_CUDA(cudaMalloc(&d_vol, nvox * sizeof(float)));
+  float *d_band, *d_slab;
+  {
+    std::lock_guard<std::mutex> lk(p.mu);
+    d_band = ensure_buffer(p.d_stage_in, p.stage_in_elems, np * per_view);
+    d_slab = ensure_buffer(p.d_stage_out, p.stage_out_elems, nvox);
+  }
   HostPipe hp(n_chunks);
   const float scale = fdk ? float(fdk_scale(p, use_parker)) : 1.0f;
   for (int c = 0; c < n_chunks; ++c) {
-    const uint64_t v0 = uint64_t(c) * chunk, vn = std::min(chunk, np - v0);
-    TG_CUDA(cudaMemcpyAsync(d_sino + v0 * per_view, h_sino + v0 * per_view,
-                            vn * per_view * sizeof(float), cudaMemcpyHostToDevice, hp.xs));
+    const uint64_t w0 = uint64_t(c) * chunk, wn = std::min(chunk, np - w0);
+    TG_CUDA(cudaMemcpyAsync(d_band + w0 * per_view, h_band + w0 * per_view,
+                            wn * per_view * sizeof(float), cudaMemcpyHostToDevice, hp.xs));
     TG_CUDA(cudaEventRecord(hp.ev[c], hp.xs));
   }
-  // K3 + K1 per chunk on the compute stream as chunks land; K1 accumulates
-  // chunk after chunk into the volume
   for (int c = 0; c < n_chunks; ++c) {
-    const uint64_t v0 = uint64_t(c) * chunk, vn = std::min(chunk, np - v0);
+    const uint64_t w0 = uint64_t(c) * chunk, wn = std::min(chunk, np - w0);
     TG_CUDA(cudaStreamWaitEvent(hp.cs, hp.ev[c], 0));
-    float* part = d_sino + v0 * per_view;
-    if (fdk) prefilter_impl(p, part, part, use_parker, 0, nv, v0, vn, hp.cs);
-    backproject_impl(p, 0, p.vol.shape[2], 0, nv, d_sino, d_vol, scale, c > 0, hp.cs, v0, vn);
+    float* part = d_band + w0 * per_view;
+    if (fdk) prefilter_impl(p, part, part, use_parker, v0, n_rows, w0, wn, hp.cs);
+    backproject_impl(p, z0, nz, v0, n_rows, d_band, d_slab, scale, c > 0, hp.cs, w0, wn);
   }
-  TG_CUDA(cudaMemcpyAsync(h_vol, d_vol, nvox * sizeof(float), cudaMemcpyDeviceToHost, hp.cs));
+  TG_CUDA(cudaMemcpyAsync(h_slab, d_slab, nvox * sizeof(float), cudaMemcpyDeviceToHost, hp.cs));
   TG_CUDA(cudaStreamSynchronize(hp.cs));
-  TG_CUDA(cudaFree(d_sino));
-  TG_CUDA(cudaFree(d_vol));
 }
 
 // Detector rows a z-slab can touch: project the slab's 8 corners on every
@@ -887,6 +926,8 @@ tg_status tg_cone_plan_destroy(tg_cone_plan* p) {
     cudaFree(p->d_parker);
     cudaFree(p->d_vpad);
     cudaFree(p->d_pitched);
+    cudaFree(p->d_stage_in);
+    cudaFree(p->d_stage_out);
     if (p->ramlak) filt::destroy(p->ramlak);
     delete p;
   });
@@ -978,11 +1019,23 @@ tg_status tg_cone_forward_host(tg_cone_plan* p, const float* h_vol, float* h_sin
 }
 
 tg_status tg_cone_backproject_host(tg_cone_plan* p, const float* h_sino, float* h_vol) {
-  return guarded([&] { host_backproject(*p, h_sino, h_vol, 0, false); });
+  return guarded([&] {
+    host_backproject(*p, 0, p->vol.shape[2], 0, p->det.n_v, h_sino, h_vol, 0, false);
+  });
+}
+
+tg_status tg_cone_backproject_slab_host(tg_cone_plan* p, uint64_t z0, uint64_t nz, uint64_t v0,
+                                        uint64_t n_rows, const float* h_band, float* h_slab,
+                                        int fdk, int use_parker) {
+  return guarded([&] {
+    host_backproject(*p, z0, nz, v0, n_rows, h_band, h_slab, fdk, use_parker != 0);
+  });
 }
 
 tg_status tg_cone_fdk_host(tg_cone_plan* p, const float* h_sino, float* h_vol, int use_parker) {
-  return guarded([&] { host_backproject(*p, h_sino, h_vol, 1, use_parker != 0); });
+  return guarded([&] {
+    host_backproject(*p, 0, p->vol.shape[2], 0, p->det.n_v, h_sino, h_vol, 1, use_parker != 0);
+  });
 }
 
 }  // extern "C"
