@@ -329,7 +329,8 @@ def main():
         e2e_step()
     e2e_s = max_over_ranks(time.perf_counter() - t0)
     e2e_value = updates_total * e2e_n / e2e_s / 1e9
-    e2e_parity = float((h_slab.to(dev) - slab).abs().max() / slab.abs().max().clamp_min(1e-30))
+    # the host call back-projects with scale 1; the timed K1 carried the FDK constant
+    e2e_parity = float((h_slab.to(dev) * scale - slab).abs().max() / slab.abs().max().clamp_min(1e-30))
 
     # ---- roofline (K1) --------------------------------------------------------
     pk = peaks()

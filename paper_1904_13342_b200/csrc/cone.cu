@@ -350,7 +350,10 @@ struct FpArgs {
   double ox, oy, oz, sx, sy, sz;
   double step;                    // march_step: 0.5 * min pitch
   const double* __restrict__ geo;  // per view: source (3) + inverse block (9)
-  const float* __restrict__ vpad;  // zero-bordered volume, +2 on each side
+  // zero-bordered "quad" volume, +2 on each side: element (x, y, z) holds
+  // (V[z][y][x], V[z][y][x+1], V[z][y+1][x], V[z][y+1][x+1]), so one
+  // trilinear sample is two 16-byte gathers (slices z and z+1)
+  const float4* __restrict__ vq;
   int nxp, nyp;                   // padded extents (x, y)
   float* out;                     // [n_views][nv][nu]
 };
@@ -395,9 +398,12 @@ __device__ __forceinline__ float lerpf(float a, float b, float w) { return fmaf(
 // of detector rows sees only a z-slab of the volume through every view, so
 // the CTAs resident at any time gather from an L2-sized working set instead
 // of streaming the whole volume from HBM once per view.
+// Each warp covers 8 u x 4 v pixels (its rays stay close together in 3D:
+// fewer cache lines per gather than a 32-wide row of pixels).
 __global__ void __launch_bounds__(256) cone_fp_kernel(const FpArgs a) {
-  const int iu = blockIdx.x * 32 + threadIdx.x;
-  const int iv = blockIdx.z * 8 + threadIdx.y;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int iu = blockIdx.x * 32 + (w & 3) * 8 + (lane & 7);
+  const int iv = blockIdx.z * 8 + (w >> 2) * 4 + (lane >> 3);
   const int vl = blockIdx.y;
   if (iu >= a.nu || iv >= a.nv) return;
   const double* g = a.geo + 12 * (a.view0 + vl);
@@ -444,7 +450,7 @@ __global__ void __launch_bounds__(256) cone_fp_kernel(const FpArgs a) {
                  az = p0z + double(k0) * ddz;
     const double cx = floor(ax), cy = floor(ay), cz = floor(az);
     const float bx = float(ax - cx), by = float(ay - cy), bz = float(az - cz);
-    const float* cell = a.vpad + (long long)cz * nxyp + (long long)cy * nxp + (long long)cx;
+    const float4* cell = a.vq + (long long)cz * nxyp + (long long)cy * nxp + (long long)cx;
     const int m = int(min(64LL, n - k0));
     float sum = 0.0f;
 #pragma unroll 2
@@ -456,19 +462,19 @@ __global__ void __launch_bounds__(256) cone_fp_kernel(const FpArgs a) {
       const float wx = px - (tx - MAGIC), wy = py - (ty - MAGIC), wz = pz - (tz - MAGIC);
       const int off = (__float_as_int(tx) - MAGIC_BITS) + (__float_as_int(ty) - MAGIC_BITS) * nxp +
                       (__float_as_int(tz) - MAGIC_BITS) * nxyp;
-      const float* b = cell + off;
-      const float c00 = lerpf(__ldg(b), __ldg(b + 1), wx);
-      const float c01 = lerpf(__ldg(b + nxp), __ldg(b + nxp + 1), wx);
-      const float c10 = lerpf(__ldg(b + nxyp), __ldg(b + nxyp + 1), wx);
-      const float c11 = lerpf(__ldg(b + nxyp + nxp), __ldg(b + nxyp + nxp + 1), wx);
-      sum += lerpf(lerpf(c00, c01, wy), lerpf(c10, c11, wy), wz);
+      const float4 q0 = __ldg(cell + off);          // slice z:   x/x+1 at y, y+1
+      const float4 q1 = __ldg(cell + off + nxyp);   // slice z+1
+      const float c0 = lerpf(lerpf(q0.x, q0.y, wx), lerpf(q0.z, q0.w, wx), wy);
+      const float c1 = lerpf(lerpf(q1.x, q1.y, wx), lerpf(q1.z, q1.w, wx), wy);
+      sum += lerpf(c0, c1, wz);
     }
     total += double(sum);
   }
   *out = float(total * dt);
 }
 
-__global__ void pad_volume_kernel(const float* __restrict__ vol, float* __restrict__ vpad, int nx,
+// builds the zero-bordered quad volume K2 gathers from (one pass over V)
+__global__ void pad_volume_kernel(const float* __restrict__ vol, float4* __restrict__ vq, int nx,
                                   int ny, int nz) {
   const int nxp = nx + 4, nyp = ny + 4, nzp = nz + 4;
   const long long total = (long long)nxp * nyp * nzp;
@@ -478,10 +484,20 @@ __global__ void pad_volume_kernel(const float* __restrict__ vol, float* __restri
     const long long r = i / nxp;
     const int py = int(r % nyp), pz = int(r / nyp);
     const int x = px - 2, y = py - 2, z = pz - 2;
-    float v = 0.0f;
-    if (x >= 0 && x < nx && y >= 0 && y < ny && z >= 0 && z < nz)
-      v = __ldg(vol + ((long long)z * ny + y) * nx + x);
-    vpad[i] = v;
+    float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (z >= 0 && z < nz) {
+      const float* s = vol + (long long)z * ny * nx;
+      const bool x0 = x >= 0 && x < nx, x1 = x + 1 >= 0 && x + 1 < nx;
+      if (y >= 0 && y < ny) {
+        if (x0) q.x = __ldg(s + (long long)y * nx + x);
+        if (x1) q.y = __ldg(s + (long long)y * nx + x + 1);
+      }
+      if (y + 1 >= 0 && y + 1 < ny) {
+        if (x0) q.z = __ldg(s + (long long)(y + 1) * nx + x);
+        if (x1) q.w = __ldg(s + (long long)(y + 1) * nx + x + 1);
+      }
+    }
+    vq[i] = q;
   }
 }
 
@@ -512,7 +528,7 @@ struct tg_cone_plan {
   double* d_parker = nullptr;  // [n_proj][n_u]
   filt::RowFilter* ramlak = nullptr;
   // scratch
-  float* d_vpad = nullptr;
+  float4* d_vpad = nullptr;  // K2 quad volume (zero border 2)
   size_t vpad_elems = 0;
   float* d_pitched = nullptr;  // band copy with a 16-byte row pitch when n_u % 4 != 0
   size_t pitched_elems = 0;
@@ -668,7 +684,7 @@ void ensure_vpad(tg_cone_plan& p) {
   const size_t need = size_t(p.vol.shape[0] + 4) * (p.vol.shape[1] + 4) * (p.vol.shape[2] + 4);
   if (p.vpad_elems >= need) return;
   if (p.d_vpad) TG_CUDA(cudaFree(p.d_vpad));
-  TG_CUDA(cudaMalloc(&p.d_vpad, need * sizeof(float)));
+  TG_CUDA(cudaMalloc(&p.d_vpad, need * sizeof(float4)));
   p.vpad_elems = need;
 }
 
@@ -700,7 +716,7 @@ void forward_impl(tg_cone_plan& p, uint64_t view0, uint64_t nviews, const float*
   m = (a.sz < m) ? a.sz : m;
   a.step = 0.5 * m;
   a.geo = p.d_geo;
-  a.vpad = p.d_vpad;
+  a.vq = p.d_vpad;
   a.nxp = nx + 4;
   a.nyp = ny + 4;
   KernelTimer timer;
@@ -711,7 +727,7 @@ void forward_impl(tg_cone_plan& p, uint64_t view0, uint64_t nviews, const float*
     a.view0 = int(view0 + c0);
     a.out = d_out + c0 * p.det.n_u * p.det.n_v;
     dim3 grid((a.nu + 31) / 32, unsigned(cn), (a.nv + 7) / 8);
-    cone_fp_kernel<<<grid, dim3(32, 8), 0, st>>>(a);
+    cone_fp_kernel<<<grid, 256, 0, st>>>(a);
     TG_LAUNCHED(1);
   }
   timer.stop();

@@ -1,0 +1,286 @@
+// fft16.cuh — K3 fast path: register radix-16 Stockham FFT row filter for
+// windows P in {512, 1024, 2048, 4096, 8192} (the BASELINE configs use 1024,
+// 2048 and 4096).
+//
+// One CTA transforms one complex row z = a + i b (two real detector rows when
+// the filter is symmetric), with P/16 threads each holding 16 complex values
+// in registers per pass:
+//   forward : [global rows (+ FDK pre-weights) -> R16] -> R16 -> R_last (x W)
+//   inverse : R16 -> R16 -> [R_last -> global, first n samples only]
+// so the zero-padding load and the truncating store are fused into the
+// first / last pass and the filter multiply into the forward's last store.
+// Shared memory is indexed with one pad word per 16 entries (bank-conflict
+// free radix-16 stores).  Twiddles come from an FP64-derived table.
+#pragma once
+
+#include <cmath>
+#include <vector>
+
+#include "filter.cuh"
+
+namespace tgb {
+namespace filt {
+namespace fft16 {
+
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+  return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
+}
+__device__ __forceinline__ float2 operator+(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ float2 operator-(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+
+__device__ __forceinline__ int pad(int i) { return i + (i >> 4); }
+
+// multiply by -i (forward) or +i (inverse)
+template <bool INV>
+__device__ __forceinline__ float2 rot(float2 d) {
+  return INV ? make_float2(-d.y, d.x) : make_float2(d.y, -d.x);
+}
+
+template <bool INV>
+__device__ __forceinline__ void dft4(float2& v0, float2& v1, float2& v2, float2& v3) {
+  const float2 t0 = v0 + v2, t1 = v0 - v2, t2 = v1 + v3, t3 = rot<INV>(v1 - v3);
+  v0 = t0 + t2;
+  v1 = t1 + t3;
+  v2 = t0 - t2;
+  v3 = t1 - t3;
+}
+
+// cos / sin of 2 pi m / 16 for m = 0..15 (exact decimal expansions)
+__host__ __device__ constexpr float cos16(int m) {
+  constexpr float c[16] = {1.0f, 0.92387953251128674f, 0.70710678118654752f, 0.38268343236508977f,
+                           0.0f, -0.38268343236508977f, -0.70710678118654752f, -0.92387953251128674f,
+                           -1.0f, -0.92387953251128674f, -0.70710678118654752f, -0.38268343236508977f,
+                           0.0f, 0.38268343236508977f, 0.70710678118654752f, 0.92387953251128674f};
+  return c[m & 15];
+}
+__host__ __device__ constexpr float sin16(int m) { return cos16(m - 4); }
+
+// W_R^m = exp(-+ 2 pi i m / R) for R | 16; m is a compile-time constant after unrolling
+template <int R, bool INV>
+__device__ __forceinline__ float2 wconst(int m) {
+  const int q = m * (16 / R);
+  return make_float2(cos16(q), INV ? sin16(q) : -sin16(q));
+}
+
+// In-place DFT of length R (2, 4, 8, 16) without temporaries: R = 4 * R2,
+// n = R2 n1 + n2, k = k1 + 4 k2.  Four-point transforms over n1 for each n2,
+// twiddle W_R^(n2 k1), then R2-point transforms over n2 for each k1.  The
+// result X[m] is left in register slot(m) = R2 (m % 4) + m / 4.
+template <int R>
+__host__ __device__ constexpr int slot(int m) {
+  return R <= 4 ? m : (R / 4) * (m % 4) + m / 4;
+}
+
+template <int R, bool INV>
+__device__ __forceinline__ void dft(float2* v) {
+  if constexpr (R == 2) {
+    const float2 t = v[0];
+    v[0] = t + v[1];
+    v[1] = t - v[1];
+  } else if constexpr (R == 4) {
+    dft4<INV>(v[0], v[1], v[2], v[3]);
+  } else {
+    constexpr int R2 = R / 4;
+#pragma unroll
+    for (int n2 = 0; n2 < R2; ++n2) {
+      dft4<INV>(v[n2], v[R2 + n2], v[2 * R2 + n2], v[3 * R2 + n2]);
+      // Y[n2][k1] now sits in v[R2 k1 + n2]
+      if (n2) {
+        v[R2 + n2] = cmul(v[R2 + n2], wconst<R, INV>(n2));
+        v[2 * R2 + n2] = cmul(v[2 * R2 + n2], wconst<R, INV>(2 * n2));
+        v[3 * R2 + n2] = cmul(v[3 * R2 + n2], wconst<R, INV>(3 * n2));
+      }
+    }
+#pragma unroll
+    for (int k1 = 0; k1 < 4; ++k1) {
+      if constexpr (R2 == 2) {
+        const float2 t = v[2 * k1];
+        v[2 * k1] = t + v[2 * k1 + 1];
+        v[2 * k1 + 1] = t - v[2 * k1 + 1];
+      } else {
+        dft4<INV>(v[4 * k1], v[4 * k1 + 1], v[4 * k1 + 2], v[4 * k1 + 3]);
+      }
+    }
+  }
+}
+
+enum { SRC_SMEM = 0, SRC_GLOBAL = 1 };
+enum { DST_SMEM = 0, DST_SMEM_FILTER = 1, DST_GLOBAL = 2 };
+
+struct RowIO {
+  const float* pa;
+  const float* pb;  // nullptr when the CTA has a single row
+  float* oa;
+  float* ob;
+  int n;
+  uint64_t ra;  // launch-relative index of row a (for pre-weights)
+  PreWeights pw;
+  const float* w;  // filter weights (DST_SMEM_FILTER)
+  float out_scale;
+};
+
+__device__ __forceinline__ float preweight(float v, const PreWeights& pw, uint64_t row, int j, int n) {
+  if (pw.cos) v = float(double(v) * __ldg(pw.cos + (pw.cos_row0 + row % pw.rows_per_view) * n + j));
+  if (pw.parker) v = float(double(v) * __ldg(pw.parker + (row / pw.rows_per_view) * n + j));
+  return v;
+}
+
+// One Stockham radix-R pass (Bainville): butterfly j reads src[j + r P/R],
+// twiddles by w_P(r k P/(Ns R)) with k = j mod Ns, writes dst[(j-k) R + k + r Ns].
+template <int P, int R, bool INV, int SRC, int DST>
+__device__ __forceinline__ void pass(const float2* __restrict__ x, float2* __restrict__ y, int Ns,
+                                     const float2* __restrict__ tw, const RowIO& io) {
+  constexpr int NB = P / R;          // butterflies
+  constexpr int T = P / 16;          // threads
+  constexpr int PER = NB / T;        // butterflies per thread (16 / R)
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    const int j = threadIdx.x + q * T;
+    const int k = j & (Ns - 1);
+    float2 v[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int i = j + r * NB;
+      if constexpr (SRC == SRC_GLOBAL) {
+        float2 z = make_float2(0.f, 0.f);
+        if (i < io.n) {
+          z.x = preweight(io.pa[i], io.pw, io.ra, i, io.n);
+          if (io.pb) z.y = preweight(io.pb[i], io.pw, io.ra + 1, i, io.n);
+        }
+        v[r] = z;
+      } else {
+        v[r] = x[pad(i)];
+      }
+    }
+    if (Ns > 1) {
+      // per-pass table [r][k] = w_P(r k P / (Ns R)): consecutive lanes read
+      // consecutive entries
+#pragma unroll
+      for (int r = 1; r < R; ++r) {
+        float2 t = __ldg(tw + r * Ns + k);
+        if (INV) t.y = -t.y;
+        v[r] = cmul(v[r], t);
+      }
+    }
+    dft<R, INV>(v);
+    const int o = (j - k) * R + k;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int i = o + r * Ns;
+      const float2 x_r = v[slot<R>(r)];
+      if constexpr (DST == DST_GLOBAL) {
+        if (i < io.n) {
+          io.oa[i] = x_r.x * io.out_scale;
+          if (io.ob) io.ob[i] = x_r.y * io.out_scale;
+        }
+      } else if constexpr (DST == DST_SMEM_FILTER) {
+        const float wk = __ldg(io.w + i);
+        y[pad(i)] = make_float2(x_r.x * wk, x_r.y * wk);
+      } else {
+        y[pad(i)] = x_r;
+      }
+    }
+  }
+}
+
+// offset of the twiddle table of the pass with span Ns (Ns = 16, 256, 4096)
+template <int P>
+__host__ __device__ constexpr int tw_offset(int Ns) {
+  return Ns == 16 ? 0 : (Ns == 256 ? 256 : 256 + 16 * 256);
+}
+// radix of the pass with span Ns
+template <int P>
+__host__ __device__ constexpr int radix_at(int Ns) {
+  return (P == 8192) ? (Ns == 4096 ? 2 : 16) : (Ns == 256 ? P / 256 : 16);
+}
+template <int P>
+__host__ __device__ constexpr int tw_table_size() {
+  return P == 8192 ? 256 + 16 * 256 + 2 * 4096 : 256 + (P / 256) * 256;
+}
+
+// occupancy target: 16 resident warps per SM (<= 128 registers per thread)
+template <int P>
+constexpr int min_blocks() {
+  return (512 / (P / 16)) < 1 ? 1 : ((512 / (P / 16)) > 16 ? 16 : (512 / (P / 16)));
+}
+
+template <int P>
+__global__ void __launch_bounds__(P / 16, min_blocks<P>()) filter_kernel(const float* in, float* out, int n,
+                                                        uint64_t n_rows, int packed,
+                                                        const float* __restrict__ w,
+                                                        const float2* __restrict__ tw,
+                                                        PreWeights pw) {
+  extern __shared__ float2 sm[];
+  constexpr int PADDED = P + P / 16;
+  float2* A = sm;
+  float2* B = sm + PADDED;
+  RowIO io;
+  io.ra = packed ? 2 * uint64_t(blockIdx.x) : uint64_t(blockIdx.x);
+  const bool has_b = packed && io.ra + 1 < n_rows;
+  io.pa = in + io.ra * uint64_t(n);
+  io.pb = has_b ? io.pa + n : nullptr;
+  io.oa = out + io.ra * uint64_t(n);
+  io.ob = has_b ? io.oa + n : nullptr;
+  io.n = n;
+  io.pw = pw;
+  io.w = w;
+  io.out_scale = 1.0f / float(P);
+  constexpr int RL = (P == 8192) ? 2 : P / 256;  // last radix
+  // forward
+  pass<P, 16, false, SRC_GLOBAL, DST_SMEM>(nullptr, A, 1, tw, io);
+  __syncthreads();
+  if constexpr (P == 8192) {
+    pass<P, 16, false, SRC_SMEM, DST_SMEM>(A, B, 16, tw + tw_offset<P>(16), io);
+    __syncthreads();
+    pass<P, 16, false, SRC_SMEM, DST_SMEM>(B, A, 256, tw + tw_offset<P>(256), io);
+    __syncthreads();
+    pass<P, 2, false, SRC_SMEM, DST_SMEM_FILTER>(A, B, 4096, tw + tw_offset<P>(4096), io);
+    __syncthreads();
+    // inverse
+    pass<P, 16, true, SRC_SMEM, DST_SMEM>(B, A, 1, tw, io);
+    __syncthreads();
+    pass<P, 16, true, SRC_SMEM, DST_SMEM>(A, B, 16, tw + tw_offset<P>(16), io);
+    __syncthreads();
+    pass<P, 16, true, SRC_SMEM, DST_SMEM>(B, A, 256, tw + tw_offset<P>(256), io);
+    __syncthreads();
+    pass<P, 2, true, SRC_SMEM, DST_GLOBAL>(A, nullptr, 4096, tw + tw_offset<P>(4096), io);
+  } else {
+    pass<P, 16, false, SRC_SMEM, DST_SMEM>(A, B, 16, tw + tw_offset<P>(16), io);
+    __syncthreads();
+    pass<P, RL, false, SRC_SMEM, DST_SMEM_FILTER>(B, A, 256, tw + tw_offset<P>(256), io);
+    __syncthreads();
+    // inverse
+    pass<P, 16, true, SRC_SMEM, DST_SMEM>(A, B, 1, tw, io);
+    __syncthreads();
+    pass<P, 16, true, SRC_SMEM, DST_SMEM>(B, A, 16, tw + tw_offset<P>(16), io);
+    __syncthreads();
+    pass<P, RL, true, SRC_SMEM, DST_GLOBAL>(A, nullptr, 256, tw + tw_offset<P>(256), io);
+  }
+}
+
+// host: per-pass twiddle tables [r][k] = exp(-2 pi i r k P/(Ns R) / P) from FP64
+template <int P>
+inline std::vector<float2> make_tw_table() {
+  std::vector<float2> t(tw_table_size<P>());
+  const int spans[3] = {16, 256, 4096};
+  for (int Ns : spans) {
+    if (Ns >= P) break;
+    const int R = radix_at<P>(Ns);
+    for (int r = 0; r < R; ++r)
+      for (int k = 0; k < Ns; ++k) {
+        const double m = double(r) * double(k) * double(P / (Ns * R));
+        const double ang = -2.0 * kPi * m / double(P);
+        t[tw_offset<P>(Ns) + r * Ns + k] = make_float2(float(std::cos(ang)), float(std::sin(ang)));
+      }
+  }
+  return t;
+}
+
+template <int P>
+inline size_t smem_bytes() {
+  return 2 * size_t(P + P / 16) * sizeof(float2);
+}
+
+}  // namespace fft16
+}  // namespace filt
+}  // namespace tgb

@@ -11,6 +11,7 @@
 #include <memory>
 #include <vector>
 
+#include "fft16.cuh"
 #include "filter.cuh"
 
 namespace tgb {
@@ -163,6 +164,19 @@ RowFilter* create(uint64_t n, uint64_t P, const double* weights, int device) {
   TG_CUDA(cudaMalloc(&f->d_tw, P * sizeof(float2)));
   TG_CUDA(cudaMemcpy(f->d_w, w.data(), P * sizeof(float), cudaMemcpyHostToDevice));
   TG_CUDA(cudaMemcpy(f->d_tw, tw.data(), P * sizeof(float2), cudaMemcpyHostToDevice));
+  std::vector<float2> t16;
+  switch (P) {
+    case 512: t16 = fft16::make_tw_table<512>(); break;
+    case 1024: t16 = fft16::make_tw_table<1024>(); break;
+    case 2048: t16 = fft16::make_tw_table<2048>(); break;
+    case 4096: t16 = fft16::make_tw_table<4096>(); break;
+    case 8192: t16 = fft16::make_tw_table<8192>(); break;
+    default: break;
+  }
+  if (!t16.empty()) {
+    TG_CUDA(cudaMalloc(&f->d_tw16, t16.size() * sizeof(float2)));
+    TG_CUDA(cudaMemcpy(f->d_tw16, t16.data(), t16.size() * sizeof(float2), cudaMemcpyHostToDevice));
+  }
   return f.release();
 }
 
@@ -170,6 +184,7 @@ void destroy(RowFilter* f) {
   if (!f) return;
   cudaFree(f->d_w);
   cudaFree(f->d_tw);
+  cudaFree(f->d_tw16);
   delete f;
 }
 
@@ -180,22 +195,30 @@ void apply(const RowFilter& f, const float* d_in, float* d_out, uint64_t n_rows,
   PreWeights w = pw ? *pw : PreWeights{};
   const bool packed = f.symmetric;
   const uint64_t blocks = packed ? (n_rows + 1) / 2 : n_rows;
-  const size_t smem = 2 * f.P * sizeof(float2);
-  TG_CUDA(cudaFuncSetAttribute(row_filter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               int(smem)));
+  check(blocks <= 2147483647ull, "too many detector rows for one filter launch");
   KernelTimer timer;
   timer.start(st);
-  for (uint64_t b0 = 0; b0 < blocks; b0 += 2147483647ull) {
-    const uint64_t nb = std::min<uint64_t>(blocks - b0, 2147483647ull);
-    const uint64_t row0 = packed ? 2 * b0 : b0;
-    PreWeights wc = w;
-    // keep row numbering relative to this launch's first row
-    if (wc.parker) wc.parker += (row0 / wc.rows_per_view) * f.n;
-    row_filter_kernel<<<unsigned(nb), kThreads, smem, st>>>(
-        d_in + row0 * f.n, d_out + row0 * f.n, int(f.n), int(f.P), n_rows - row0, packed, f.d_w,
-        f.d_tw, wc);
-    TG_LAUNCHED(1);
+  const int n = int(f.n);
+  auto launch16 = [&](auto kern, int P, size_t smem) {
+    TG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    kern<<<unsigned(blocks), P / 16, smem, st>>>(d_in, d_out, n, n_rows, int(packed), f.d_w, f.d_tw16,
+                                                  w);
+  };
+  switch (f.P) {
+    case 512: launch16(fft16::filter_kernel<512>, 512, fft16::smem_bytes<512>()); break;
+    case 1024: launch16(fft16::filter_kernel<1024>, 1024, fft16::smem_bytes<1024>()); break;
+    case 2048: launch16(fft16::filter_kernel<2048>, 2048, fft16::smem_bytes<2048>()); break;
+    case 4096: launch16(fft16::filter_kernel<4096>, 4096, fft16::smem_bytes<4096>()); break;
+    case 8192: launch16(fft16::filter_kernel<8192>, 8192, fft16::smem_bytes<8192>()); break;
+    default: {  // small windows: generic radix-4 shared-memory transform
+      const size_t smem = 2 * f.P * sizeof(float2);
+      TG_CUDA(cudaFuncSetAttribute(row_filter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   int(smem)));
+      row_filter_kernel<<<unsigned(blocks), kThreads, smem, st>>>(d_in, d_out, n, int(f.P), n_rows,
+                                                                  packed, f.d_w, f.d_tw, w);
+    }
   }
+  TG_LAUNCHED(1);
   timer.stop();
 }
 

@@ -16,6 +16,7 @@ struct RowFilter {
   bool symmetric = true;   // W[k] == W[P-k]: two real rows share one complex FFT
   float* d_w = nullptr;    // P real weights (fp32)
   float2* d_tw = nullptr;  // P twiddles exp(-2 pi i k / P) (from FP64)
+  float2* d_tw16 = nullptr;  // per-pass [r][k] twiddle tables of the radix-16 path
 };
 
 // Optional per-element weights applied (in FP64, rounded to fp32 after each
