@@ -1,0 +1,182 @@
+// shim_test.cpp — drop-in check: the reference's own headers (pipelines.hpp,
+// graph.hpp, filtering.hpp, ...) compiled against OUR tomograd/projector.hpp
+// (include/tomograd_b200/tomograd/projector.hpp), so every reference caller
+// of forward_project / back_project runs the B200 kernels.  Results are
+// compared with the CPU oracle (oracle/liboracle.so, plain C).
+//
+// Built by __graft_entry__.build() where /root/reference is mounted
+// (build/shim_test); run on a GPU box by tests/test_gpu_shim.py.
+#include <cmath>
+#include <cstdio>
+#include <numbers>
+#include <string>
+#include <vector>
+
+#include "tomograd/projector.hpp"  // ours: must come first
+#include "tomograd/pipelines.hpp"   // the reference's, calling ours
+#include "tg_oracle.h"
+
+using namespace tomograd;
+
+namespace {
+
+int failures = 0;
+
+void report(const char* name, bool ok, const std::string& detail = "") {
+  std::printf("%s %s %s\n", ok ? "PASS" : "FAIL", name, detail.c_str());
+  if (!ok) ++failures;
+}
+
+template <typename A, typename B>
+std::pair<double, double> rel_err(const std::vector<A>& out, const std::vector<B>& ref) {
+  double dmax = 0, rmax = 0, d2 = 0, r2 = 0;
+  for (std::size_t i = 0; i < ref.size(); ++i) {
+    const double d = double(out[i]) - double(ref[i]);
+    dmax = std::max(dmax, std::abs(d));
+    rmax = std::max(rmax, std::abs(double(ref[i])));
+    d2 += d * d;
+    r2 += double(ref[i]) * double(ref[i]);
+  }
+  return {rmax > 0 ? dmax / rmax : dmax, r2 > 0 ? std::sqrt(d2 / r2) : std::sqrt(d2)};
+}
+
+bool close(const char* name, std::pair<double, double> e, double rmse = 1e-5, double mx = 1e-4) {
+  char buf[160];
+  std::snprintf(buf, sizeof buf, "max_rel=%.3g rel_rmse=%.3g", e.first, e.second);
+  const bool ok = e.second <= rmse && e.first <= mx;
+  report(name, ok, buf);
+  return ok;
+}
+
+or_volume ov(const VolumeSpec& v) {
+  or_volume o{};
+  o.dims = uint32_t(v.shape.size());
+  for (std::size_t a = 0; a < v.shape.size(); ++a) {
+    o.shape[a] = v.shape[a];
+    o.spacing[a] = v.spacing[a];
+    o.origin[a] = v.origin[a];
+  }
+  return o;
+}
+
+struct OracleCone {
+  std::vector<double> mats, src, inv, ang;
+  or_cone g{};
+  explicit OracleCone(const ConeGeometry& geo) {
+    for (auto& m : geo.matrices) mats.insert(mats.end(), m.m.begin(), m.m.end());
+    for (auto& s : geo.sources) src.insert(src.end(), {s.x, s.y, s.z});
+    for (auto& b : geo.inv_blocks) inv.insert(inv.end(), b.m.begin(), b.m.end());
+    ang = geo.angles;
+    g.vol = ov(geo.volume);
+    g.det = {geo.detector.n_u, geo.detector.n_v, geo.detector.spacing_u, geo.detector.spacing_v,
+             geo.detector.origin_u, geo.detector.origin_v};
+    g.n_proj = geo.n_projections;
+    g.range = geo.angular_range;
+    g.sid = geo.sid;
+    g.sdd = geo.sdd;
+    g.mats = mats.data();
+    g.sources = src.data();
+    g.invs = inv.data();
+    g.angles = ang.data();
+  }
+};
+
+}  // namespace
+
+int main() {
+  const double pi = std::numbers::pi;
+  // shipped FDK short-scan geometry (configs/fdk_short_scan_geometry.json)
+  auto vol = VolumeSpec::centered({64, 64, 64}, {0.85, 0.85, 0.85});
+  auto det = Detector2D::centered(96, 96, 1.0, 1.0);
+  auto geo = make_cone(vol, det, 248, 200.0 * pi / 180.0, 750.0, 1200.0);
+  OracleCone oc(geo);
+  auto ph = shepp_logan_3d<float>(vol);
+
+  // forward projection through the drop-in header
+  auto sino = forward_project(ph, geo);
+  std::vector<float> ref_sino(sino.data.size());
+  or_cone_forward_f32(&oc.g, ph.data.data(), ref_sino.data());
+  close("cone_forward_project<float>", rel_err(sino.data, ref_sino));
+
+  // back projection
+  auto bp = back_project(sino, geo);
+  std::vector<float> ref_bp(bp.data.size());
+  or_cone_backproject_f32(&oc.g, sino.data.data(), ref_bp.data());
+  close("cone_back_project<float>", rel_err(bp.data, ref_bp));
+
+  // the reference's own fdk_reconstruct (host weights + filter) calling our BP
+  std::vector<float> ref_fdk(bp.data.size());
+  or_fdk_reconstruct_f32(&oc.g, sino.data.data(), ref_fdk.data(), 1);
+  auto rec = fdk_reconstruct(sino, geo, true);
+  close("reference fdk_reconstruct -> B200 back_project", rel_err(rec.data, ref_fdk));
+
+  // the fully-device FDK
+  auto rec2 = b200::fdk_reconstruct(sino, geo, true);
+  close("b200::fdk_reconstruct", rel_err(rec2.data, ref_fdk));
+
+  // T = double through the shim (device computes fp32)
+  auto phd = shepp_logan_3d<double>(vol);
+  auto sinod = forward_project(phd, geo);
+  close("cone_forward_project<double>", rel_err(sinod.data, ref_sino));
+
+  // parallel FBP (pipelines.hpp:49-63) and fan operators
+  auto v2 = VolumeSpec::centered({128, 128}, {1.0, 1.0});
+  auto pg = make_parallel(v2, Detector1D::centered(183, 1.0), 180, pi);
+  auto ph2 = shepp_logan_2d<float>(v2);
+  auto ps = forward_project(ph2, pg);
+  auto fbp = fbp_reconstruct(ps, pg);
+  {
+    std::vector<double> rays, ang = pg.angles;
+    for (auto& r : pg.rays) rays.insert(rays.end(), {r.x, r.y});
+    or_planar og{ov(v2), {183, 1.0, pg.detector.origin}, 180, pi, 0.0, 0.0, rays.data(), ang.data()};
+    std::vector<float> rs(ps.data.size()), rf(fbp.data.size());
+    or_parallel_forward_f32(&og, ph2.data.data(), rs.data());
+    close("parallel forward_project", rel_err(ps.data, rs));
+    const uint64_t P = or_filter_window(183);
+    std::vector<double> w(P);
+    or_ramlak_weights(P, 1.0, w.data());
+    or_fbp_reconstruct_f32(&og, ps.data.data(), rf.data(), w.data(), P);
+    close("reference fbp_reconstruct -> B200 back_project", rel_err(fbp.data, rf));
+  }
+  auto fg = make_fan(v2, Detector1D::centered(256, 1.0), 120, 2 * pi, 300.0, 600.0);
+  auto fs = forward_project(ph2, fg);
+  auto fb = back_project(fs, fg);
+  {
+    std::vector<double> rays, ang = fg.angles;
+    for (auto& r : fg.rays) rays.insert(rays.end(), {r.x, r.y});
+    or_planar og{ov(v2), {256, 1.0, fg.detector.origin}, 120, 2 * pi, 300.0, 600.0, rays.data(),
+                 ang.data()};
+    std::vector<float> rs(fs.data.size()), rb(fb.data.size());
+    or_fan_forward_f32(&og, ph2.data.data(), rs.data());
+    or_fan_backproject_f32(&og, fs.data.data(), rb.data());
+    close("fan forward_project", rel_err(fs.data, rs));
+    close("fan back_project", rel_err(fb.data, rb));
+  }
+
+  // the reference's autodiff graph (T = double) driving the B200 operators:
+  // a few gradient steps of its TV reconstruction must reduce the loss
+  {
+    ExperimentConfig cfg;
+    cfg.iterations = 5;
+    cfg.learning_rate = 1e-3;
+    cfg.tv_lambda = 0.01;
+    auto v3 = VolumeSpec::centered({48, 48}, {1.0, 1.0});
+    auto g3 = make_parallel(v3, Detector1D::centered(69, 1.0), 60, pi);
+    auto s3 = forward_project(shepp_logan_2d<double>(v3), g3);
+    auto [img, hist] = tv_reconstruct(s3, g3, cfg);
+    report("reference graph tv_reconstruct on B200 operators", hist.back() < hist.front(),
+           "loss " + std::to_string(hist.front()) + " -> " + std::to_string(hist.back()));
+  }
+
+  // error text passes through unchanged
+  try {
+    Sinogram<float> bad = Sinogram<float>::planar(3, Detector1D::centered(8, 1.0));
+    back_project(bad, geo);
+    report("error text", false, "no throw");
+  } catch (const Error& e) {
+    report("error text", std::string(e.what()) == "sinogram shape does not match the geometry",
+           e.what());
+  }
+  std::printf("%s: %d failure(s)\n", failures ? "FAILED" : "OK", failures);
+  return failures ? 1 : 0;
+}
