@@ -158,7 +158,9 @@ int main() {
   {
     ExperimentConfig cfg;
     cfg.iterations = 5;
-    cfg.learning_rate = 1e-3;
+    // stable step for ||A^T A|| ~ n_views * n at this size (1e-3 diverges on
+    // the reference's CPU operators as well)
+    cfg.learning_rate = 1e-5;
     cfg.tv_lambda = 0.01;
     auto v3 = VolumeSpec::centered({48, 48}, {1.0, 1.0});
     auto g3 = make_parallel(v3, Detector1D::centered(69, 1.0), 60, pi);
