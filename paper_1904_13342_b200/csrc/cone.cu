@@ -117,6 +117,15 @@ __global__ void footprint_kernel(BpArgs a, int K, int tiles_x, int tiles_y, int 
 // ---------------------------------------------------------------------------
 // K1: voxel-driven back-projection
 
+// d = a * B + c as one IMAD the compiler cannot re-associate (keeps the
+// per-view constant folded into c)
+template <uint32_t B>
+__device__ __forceinline__ uint32_t mad_u32(uint32_t a, uint32_t c) {
+  uint32_t d;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "n"(B), "r"(c));
+  return d;
+}
+
 // the four bilinear taps (row r: a0 a1, row r+1: b0 b1) at one shared
 // address with immediate offsets
 template <uint32_t ROWB>
@@ -161,8 +170,9 @@ struct StageHdr {
   int4 meta;  // ub, vb, mode, -
 };
 
+// 3 CTAs (27 warps) per SM: 72 registers, no spills (ptxas -v)
 template <int K, int BOXU, bool CIRC>
-__global__ void __launch_bounds__(NTHREADS, 2)
+__global__ void __launch_bounds__(NTHREADS, 3)
     cone_bp_kernel(const __grid_constant__ CUtensorMap tmap, const BpArgs a) {
   extern __shared__ __align__(128) unsigned char smem[];
   const int box_elems = BOXU * a.boxV;
@@ -280,17 +290,24 @@ __global__ void __launch_bounds__(NTHREADS, 2)
         const float v0 = fmaf(V.z, dz0, vn) * r;
         const float dv = V.z * sz * r;
         const uint32_t cbase = sbase + uint32_t(int(fu)) * 4u - MAGIC_BITS * ROWB;
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-          const float vk = fmaf(float(min(k, kmax)), dv, v0);
+        // one update: v, floor (round-down magic add), one IMAD address, 4 LDS,
+        // three lerps, one FFMA
+        auto update = [&](float kf, float& acc_k) {
+          const float vk = fmaf(kf, dv, v0);
           const float t = __fadd_rd(vk, MAGIC);
           const float wv = vk - (t - MAGIC);
-          const uint32_t ad = cbase + __float_as_uint(t) * ROWB;
           float a0, a1, b0, b1;
-          lds_quad<ROWB>(ad, a0, a1, b0, b1);
+          lds_quad<ROWB>(mad_u32<ROWB>(__float_as_uint(t), cbase), a0, a1, b0, b1);
           const float top = fmaf(wu, a1 - a0, a0);
           const float bot = fmaf(wu, b1 - b0, b0);
-          acc[k] = fmaf(fmaf(wv, bot - top, top), invw2, acc[k]);
+          acc_k = fmaf(fmaf(wv, bot - top, top), invw2, acc_k);
+        };
+        if (kmax == K - 1) {  // full tile (every tile when nz % K == 0)
+#pragma unroll
+          for (int k = 0; k < K; ++k) update(float(k), acc[k]);
+        } else {
+#pragma unroll
+          for (int k = 0; k < K; ++k) update(float(min(k, kmax)), acc[k]);
         }
       } else {
         // general calibrated matrices: full projective map per voxel
@@ -453,6 +470,12 @@ __global__ void __launch_bounds__(256) cone_fp_kernel(const FpArgs a) {
     const float4* cell = a.vq + (long long)cz * nxyp + (long long)cy * nxp + (long long)cx;
     const int m = int(min(64LL, n - k0));
     float sum = 0.0f;
+    // samples advance by at most half a voxel, so consecutive samples often
+    // stay in the same trilinear cell: re-gather only when the cell changes
+    // (lanes that keep their cell are masked off the load and cost no L1
+    // wavefronts; K2 is bound by the L1 data pipe)
+    int prev = 0x7fffffff;
+    float4 q0 = make_float4(0.f, 0.f, 0.f, 0.f), q1 = q0;
 #pragma unroll 2
     for (int j = 0; j < m; ++j) {
       const float px = fmaf(float(j), fdx, bx);
@@ -462,8 +485,11 @@ __global__ void __launch_bounds__(256) cone_fp_kernel(const FpArgs a) {
       const float wx = px - (tx - MAGIC), wy = py - (ty - MAGIC), wz = pz - (tz - MAGIC);
       const int off = (__float_as_int(tx) - MAGIC_BITS) + (__float_as_int(ty) - MAGIC_BITS) * nxp +
                       (__float_as_int(tz) - MAGIC_BITS) * nxyp;
-      const float4 q0 = __ldg(cell + off);          // slice z:   x/x+1 at y, y+1
-      const float4 q1 = __ldg(cell + off + nxyp);   // slice z+1
+      if (off != prev) {
+        q0 = __ldg(cell + off);         // slice z:   x/x+1 at y, y+1
+        q1 = __ldg(cell + off + nxyp);  // slice z+1
+        prev = off;
+      }
       const float c0 = lerpf(lerpf(q0.x, q0.y, wx), lerpf(q0.z, q0.w, wx), wy);
       const float c1 = lerpf(lerpf(q1.x, q1.y, wx), lerpf(q1.z, q1.w, wx), wy);
       sum += lerpf(c0, c1, wz);
@@ -610,7 +636,7 @@ void size_box(tg_cone_plan& p) {
   p.boxU = pick_boxu(std::max(need[0], 1));
   p.boxV = std::min(std::max(need[1], 2), 256);
   // keep the stage ring within ~96 KB so two CTAs fit per SM
-  while (p.boxV > 2 && size_t(STAGES) * p.boxU * p.boxV * 4 > 96 * 1024) --p.boxV;
+  while (p.boxV > 2 && size_t(STAGES) * p.boxU * p.boxV * 4 > 72 * 1024) --p.boxV;
 }
 
 // Back-project views [view0, view0 + n_views) of the band buffer (which holds
