@@ -219,10 +219,19 @@ def main():
     from paper_1904_13342_b200 import distributed as D
 
     rank, world, local = env_rank()
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    n_dev = torch.cuda.device_count()
+    gpu = local % n_dev
+    torch.cuda.set_device(gpu)
+    dev = torch.device("cuda", gpu)
+    # one process per GPU over NCCL; more ranks than GPUs (a launcher smoke
+    # test on a single-GPU box) falls back to gloo for the control plane only
+    # (the data path has no collective)
+    backend = "nccl" if world <= n_dev else "gloo"
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
     L = tg._native.lib()
     geo = c4_geometry(tg)
     shards = D.slab_shards(geo, world)
@@ -238,7 +247,7 @@ def main():
     def max_over_ranks(x):
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        t = torch.tensor([x], dtype=torch.float64, device=dev if backend == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -260,7 +269,7 @@ def main():
     launches0 = int(L.tg_kernel_launch_count())
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(args.steps)]
-    with ClockSampler(local) as clk:
+    with ClockSampler(gpu) as clk:
         torch.cuda.synchronize()
         barrier()
         t_start = torch.cuda.Event(enable_timing=True)
@@ -313,7 +322,7 @@ def main():
     h_band = torch.empty(band.shape, dtype=torch.float32, pin_memory=True)
     h_band.copy_(band.cpu())
     h_slab = torch.empty(slab.shape, dtype=torch.float32, pin_memory=True)
-    plan = geo._plan(local)
+    plan = geo._plan(gpu)
 
     def e2e_step():
         tg._native.check(L.tg_cone_backproject_slab_host(plan, me.z0, me.nz, me.v0, me.n_rows,

@@ -7,6 +7,12 @@ import numpy as np
 # relative RMSE and max |d| relative to max |ref|.
 REL_RMSE = 1e-5
 REL_MAX = 1e-4
+# The standalone row filter (K3) on smooth projections: the Ram-Lak taps sum
+# to zero, so the filtered row is a cancellation much smaller than its input
+# and fp32 FFT rounding (~eps log2 P |x|) is amplified relative to |y|; the
+# reference does this in complex double.  Stated bound for the filter output
+# alone; FDK volumes (after the 1/w^2 sum over views) meet REL_RMSE.
+FILTER_REL_RMSE = 5e-5
 
 
 def cone_pair(tg, O, vshape, vsp, nu, nv, du, dv, n, rng, sid, sdd, origin=None):
