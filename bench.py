@@ -8,7 +8,7 @@ over 220 deg, SID 750 / SDD 1200, FDK short scan (Parker + Ram-Lak, P = 4096).
 One step = one K1 cone back-projection (projector.hpp:283-313) of the
 FDK-filtered projections of this rank's z-slab: the headline metric is BP
 GUPS = voxel-updates / s over the whole job.  Under torchrun each rank owns a
-16-aligned z-slab and only the detector row band it projects onto (no
+32-aligned z-slab and only the detector row band it projects onto (no
 data-path collective: SURVEY §8e); per-GPU work shrinks with N, so scaling is
 "strong".  Also reported: the forward projector K2 (Gsamples/s, exact
 per-ray sample counts of the reference's clip + ceil rule), the K3 row

@@ -151,7 +151,7 @@ tg_status tg_cone_backproject(tg_cone_plan* plan, const float* d_sino, float* d_
 /* z-slab back-projection for multi-GPU sharding: voxels z in [z0, z0+nz)
  * from detector rows [v0, v0+n_rows) of every view (d_band
  * [n_proj][n_rows][n_u]) into d_slab [nz][ny][nx].  Coordinates come from
- * global indices; when z0 and z0+nz are multiples of 16 (K1's z tile) or nz
+ * global indices; when z0 and z0+nz are multiples of 32 (K1's z tile) or nz
  * reaches the volume's end, the slab is bitwise equal to the same z range of
  * the full-volume result.  The band must cover tg_cone_slab_rows(). */
 tg_status tg_cone_slab_rows(tg_cone_plan* plan, uint64_t z0, uint64_t nz, uint64_t* v0,

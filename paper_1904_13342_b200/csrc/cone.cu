@@ -172,7 +172,7 @@ struct StageHdr {
 
 // 3 CTAs (27 warps) per SM: 72 registers, no spills (ptxas -v)
 template <int K, int BOXU, bool CIRC>
-__global__ void __launch_bounds__(NTHREADS, 3)
+__global__ void __launch_bounds__(NTHREADS, (K <= 16 ? 3 : 2))
     cone_bp_kernel(const __grid_constant__ CUtensorMap tmap, const BpArgs a) {
   extern __shared__ __align__(128) unsigned char smem[];
   const int box_elems = BOXU * a.boxV;
@@ -548,6 +548,7 @@ struct tg_cone_plan {
   double* d_mats = nullptr;   // 12 x n_proj FP64 matrices (K1's constant bank source)
   double* d_geo = nullptr;    // 12 x n_proj: source + inverse block (FP64)
   int boxV = 0, boxU = 0;     // K1 TMA box
+  int k1_k = 16;              // K1 z voxels per thread
   int need_w = 0, need_h = 0;
   // FDK pre-processing
   double* d_cos = nullptr;     // [n_v][n_u]
@@ -567,10 +568,16 @@ struct tg_cone_plan {
 
 namespace {
 
-constexpr int kK = 16;  // z voxels per K1 thread
+// z voxels per K1 thread: 32 (default: half the per-view overhead per update
+// of K = 16, 2 CTAs/SM; +10% at c4) or 16 (3 CTAs/SM); env TG_K1_K overrides
+// at plan creation.  Slabs aligned to 32 are bitwise equal to the full volume.
+int default_k1_k() {
+  const char* e = std::getenv("TG_K1_K");
+  return (e && std::atoi(e) == 16) ? 16 : 32;
+}
 
 int pick_boxu(int need) {
-  static const int choices[] = {16, 48, 80, 112, 144, 176, 208, 240};
+  static const int choices[] = {48, 80, 112, 176, 240};
   for (int c : choices)
     if (need <= c) return c;
   return 240;
@@ -600,17 +607,25 @@ void launch_bp_t(const CUtensorMap& map, const BpArgs& a, size_t smem, cudaStrea
   fn<<<grid, NTHREADS, smem, st>>>(map, a);
 }
 
-template <bool CIRC>
+template <int K, bool CIRC>
 void launch_bp_u(int boxU, const CUtensorMap& map, const BpArgs& a, size_t smem, cudaStream_t st) {
   switch (boxU) {
-    case 16: return launch_bp_t<kK, 16, CIRC>(map, a, smem, st);
-    case 48: return launch_bp_t<kK, 48, CIRC>(map, a, smem, st);
-    case 80: return launch_bp_t<kK, 80, CIRC>(map, a, smem, st);
-    case 112: return launch_bp_t<kK, 112, CIRC>(map, a, smem, st);
-    case 144: return launch_bp_t<kK, 144, CIRC>(map, a, smem, st);
-    case 176: return launch_bp_t<kK, 176, CIRC>(map, a, smem, st);
-    case 208: return launch_bp_t<kK, 208, CIRC>(map, a, smem, st);
-    default: return launch_bp_t<kK, 240, CIRC>(map, a, smem, st);
+    case 48: return launch_bp_t<K, 48, CIRC>(map, a, smem, st);
+    case 80: return launch_bp_t<K, 80, CIRC>(map, a, smem, st);
+    case 112: return launch_bp_t<K, 112, CIRC>(map, a, smem, st);
+    case 176: return launch_bp_t<K, 176, CIRC>(map, a, smem, st);
+    default: return launch_bp_t<K, 240, CIRC>(map, a, smem, st);
+  }
+}
+
+void launch_bp(int k, bool circ, int boxU, const CUtensorMap& map, const BpArgs& a, size_t smem,
+               cudaStream_t st) {
+  if (k == 32) {
+    if (circ) launch_bp_u<32, true>(boxU, map, a, smem, st);
+    else launch_bp_u<32, false>(boxU, map, a, smem, st);
+  } else {
+    if (circ) launch_bp_u<16, true>(boxU, map, a, smem, st);
+    else launch_bp_u<16, false>(boxU, map, a, smem, st);
   }
 }
 
@@ -619,6 +634,7 @@ void size_box(tg_cone_plan& p) {
   BpArgs a;
   cone_args_base(p, a);
   a.n_views = int(p.n_proj);
+  const int kK = p.k1_k;
   const int tx = (a.nx + BX - 1) / BX, ty = (a.ny + BY - 1) / BY, tz = (a.nz + kK - 1) / kK;
   int* d_need = nullptr;
   TG_CUDA(cudaMalloc(&d_need, 2 * sizeof(int)));
@@ -635,8 +651,9 @@ void size_box(tg_cone_plan& p) {
   p.need_h = need[1];
   p.boxU = pick_boxu(std::max(need[0], 1));
   p.boxV = std::min(std::max(need[1], 2), 256);
-  // keep the stage ring within ~96 KB so two CTAs fit per SM
-  while (p.boxV > 2 && size_t(STAGES) * p.boxU * p.boxV * 4 > 72 * 1024) --p.boxV;
+  // keep the stage ring small enough for 3 (K = 16) or 2 (K = 32) CTAs per SM
+  const size_t cap = (p.k1_k <= 16 ? 72 : 108) * 1024;
+  while (p.boxV > 2 && size_t(STAGES) * p.boxU * p.boxV * 4 > cap) --p.boxV;
 }
 
 // Back-project views [view0, view0 + n_views) of the band buffer (which holds
@@ -698,8 +715,7 @@ void backproject_impl(tg_cone_plan& p, uint64_t z0, uint64_t nz, uint64_t v0, ui
     // bank content key: (plan, first view, view count)
     g_bank.acquire(p.device, (p.id << 40) ^ (c0 << 20) ^ cn, st, c_views, p.d_mats + 12 * c0,
                    cn * 12 * sizeof(double));
-    if (p.circular) launch_bp_u<true>(p.boxU, map, a, smem, st);
-    else launch_bp_u<false>(p.boxU, map, a, smem, st);
+    launch_bp(p.k1_k, p.circular, p.boxU, map, a, smem, st);
     TG_LAUNCHED(1);
     g_bank.release(p.device, st);
   }
@@ -952,6 +968,7 @@ tg_status tg_cone_plan_create(const tg_cone_geometry* g, int device, tg_cone_pla
     TG_CUDA(cudaMemcpy(p->d_mats, g->matrices, 12 * n * sizeof(double), cudaMemcpyHostToDevice));
     TG_CUDA(cudaMalloc(&p->d_geo, geo.size() * sizeof(double)));
     TG_CUDA(cudaMemcpy(p->d_geo, geo.data(), geo.size() * sizeof(double), cudaMemcpyHostToDevice));
+    p->k1_k = default_k1_k();
     size_box(*p);
     *out = p.release();
   });

@@ -4,7 +4,7 @@
   the detector row band its slab projects onto (``slab_rows``), filters that
   band locally (the Ram-Lak filter runs along u) and back-projects it: single
   pass FDK has no data-path collective at all.  Slab boundaries are aligned
-  to K1's 16-voxel z tiles so a slab is bitwise equal to the same z range of
+  to K1's 32-voxel z tiles so a slab is bitwise equal to the same z range of
   the single-GPU result.
 * Forward projection shards by angle: every rank holds the volume and
   projects its view range.
@@ -24,7 +24,7 @@ import torch.distributed as dist
 from . import _native as N
 from .geometry import ConeGeometry
 
-Z_ALIGN = 16  # K1 z tile (csrc/cone.cu kK)
+Z_ALIGN = 32  # K1 z tile (csrc/cone.cu default_k1_k)
 
 
 def even_partition(n: int, parts: int, align: int = 1) -> List[Tuple[int, int]]:

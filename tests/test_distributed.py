@@ -1,5 +1,5 @@
 """Multi-process sharding logic on CPU (gloo, world_size 2): each rank owns a
-16-aligned z-slab and only the detector row band its slab projects onto,
+32-aligned z-slab and only the detector row band its slab projects onto,
 back-projects it (CPU oracle standing in for K1), and the slabs are
 all_gathered; the result must equal the single-process full volume.  The
 forward projector shards by angle and gathers views the same way."""

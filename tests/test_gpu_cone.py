@@ -123,17 +123,17 @@ def test_cone_scale_and_accumulate(tg, O):
     assert_close(out.cpu().numpy(), 1.0 + 0.5 * ref, what="scale+accumulate")
 
 
-@pytest.mark.parametrize("z0,nz", [(0, 16), (16, 16), (32, 32), (48, 16), (5, 21)])
+@pytest.mark.parametrize("z0,nz", [(0, 32), (16, 16), (32, 32), (48, 16), (5, 21)])
 def test_cone_slab_band(tg, O, z0, nz):
     """z-slab back-projection from only its detector row band equals the same
-    z range of the full-volume result (bitwise when 16-aligned)."""
+    z range of the full-volume result (bitwise when aligned to K1's 32-voxel z tile)."""
     geo, og = cone_pair(tg, O, **SHIPPED)
     s = rand(og.sino_shape, 3, -1.0, 1.0)
     full = _bp(tg, geo, s)
     v0, nr = tg.cone_slab_rows(geo, z0, nz)
     band = torch.from_numpy(np.ascontiguousarray(s[:, v0:v0 + nr, :])).to(DEV)
     slab = tg.cone_backproject_slab(geo, band, z0, nz, v0).cpu().numpy()
-    if z0 % 16 == 0 and (nz % 16 == 0 or z0 + nz == 64):
+    if z0 % 32 == 0 and (nz % 32 == 0 or z0 + nz == 64):  # K1's z tile
         assert np.array_equal(slab, full[z0:z0 + nz])
     else:
         assert_close(slab, full[z0:z0 + nz], what="unaligned slab")
