@@ -98,7 +98,9 @@ def test_slab_rows_cover_slab(tg, O):
     vol = tg.VolumeSpec.centered([64, 64, 64], [0.85] * 3)
     det = tg.Detector2D.centered(96, 96, 1.0, 1.0)
     g = tg.make_cone(vol, det, 31, 2 * math.pi, 750.0, 1200.0)
-    for sh in D.slab_shards(g, 4):
+    shards = D.slab_shards(g, 2)
+    assert [s.nz for s in shards] == [32, 32]
+    for sh in shards:
         zs = np.arange(sh.z0, sh.z0 + sh.nz)
         xs = vol.origin[0] + np.arange(64) * vol.spacing[0]
         Z = vol.origin[2] + zs * vol.spacing[2]
