@@ -265,9 +265,11 @@ __global__ void __launch_bounds__(NTHREADS, (K <= 16 ? 3 : 2))
   constexpr float MAGIC = 12582912.0f;  // 1.5 * 2^23: t = M + floor(v) under round-down
   constexpr uint32_t MAGIC_BITS = 0x4B400000u;
 
-  float acc[K];
+  // accumulators as (k, k + K/2) pairs for the FP32x2 pipe
+  float2 acc[K / 2];
 #pragma unroll
-  for (int k = 0; k < K; ++k) acc[k] = 0.0f;
+  for (int k = 0; k < K / 2; ++k) acc[k] = make_float2(0.0f, 0.0f);
+#define ACC(k) ((k) >= K / 2 ? acc[(k) - K / 2].y : acc[(k)].x)
 
   for (int it = 0; it < a.n_views; ++it) {
     const int s = it % STAGES;
@@ -289,25 +291,42 @@ __global__ void __launch_bounds__(NTHREADS, (K <= 16 ? 3 : 2))
         const float wu = u - fu;
         const float v0 = fmaf(V.z, dz0, vn) * r;
         const float dv = V.z * sz * r;
-        const uint32_t cbase = sbase + uint32_t(int(fu)) * 4u - MAGIC_BITS * ROWB;
-        // one update: v, floor (round-down magic add), one IMAD address, 4 LDS,
-        // three lerps, one FFMA
-        auto update = [&](float kf, float& acc_k) {
-          const float vk = fmaf(kf, dv, v0);
-          const float t = __fadd_rd(vk, MAGIC);
-          const float wv = vk - (t - MAGIC);
-          float a0, a1, b0, b1;
-          lds_quad<ROWB>(mad_u32<ROWB>(__float_as_uint(t), cbase), a0, a1, b0, b1);
-          const float top = fmaf(wu, a1 - a0, a0);
-          const float bot = fmaf(wu, b1 - b0, b0);
-          acc_k = fmaf(fmaf(wv, bot - top, top), invw2, acc_k);
+        // a.magic_row_off = -MAGIC_BITS * ROWB (run-time value: ptxas would
+        // otherwise re-associate the constant out of the IMAD and re-add it
+        // before every LDS — it does not fit the 24-bit immediate offset)
+        const uint32_t cbase = sbase + uint32_t(int(fu)) * 4u + a.magic_row_off;
+        // two updates per step on the packed FP32x2 pipe (FFMA2 / FADD2):
+        // voxels k and k + K/2, whose v differ by the per-view constant
+        // (K/2)·dv folded into the pair's base.  Per update: v, floor
+        // (round-down magic add), one IMAD address, 4 LDS, three lerps, one FFMA.
+        constexpr int H = K / 2;
+        const float2 v02 = make_float2(v0, fmaf(float(H), dv, v0)), dv2 = make_float2(dv, dv);
+        const float2 wu2 = make_float2(wu, wu), iw2 = make_float2(invw2, invw2);
+        const float2 M2 = make_float2(MAGIC, MAGIC), nM2 = make_float2(-MAGIC, -MAGIC);
+        auto update2 = [&](float2 vk, float2& acc2) {
+          const float2 t = __fadd2_rd(vk, M2);
+          const float2 fl = __fadd2_rn(t, nM2);
+          const float2 wv = __fadd2_rn(vk, make_float2(-fl.x, -fl.y));
+          float a0, a1, b0, b1, c0, c1, d0, d1;
+          lds_quad<ROWB>(mad_u32<ROWB>(__float_as_uint(t.x), cbase), a0, a1, b0, b1);
+          lds_quad<ROWB>(mad_u32<ROWB>(__float_as_uint(t.y), cbase), c0, c1, d0, d1);
+          const float2 p0 = make_float2(a0, c0), p1 = make_float2(a1, c1);
+          const float2 q0 = make_float2(b0, d0), q1 = make_float2(b1, d1);
+          const float2 top = __ffma2_rn(wu2, __fadd2_rn(p1, make_float2(-p0.x, -p0.y)), p0);
+          const float2 bot = __ffma2_rn(wu2, __fadd2_rn(q1, make_float2(-q0.x, -q0.y)), q0);
+          const float2 mid = __ffma2_rn(wv, __fadd2_rn(bot, make_float2(-top.x, -top.y)), top);
+          acc2 = __ffma2_rn(mid, iw2, acc2);
         };
         if (kmax == K - 1) {  // full tile (every tile when nz % K == 0)
 #pragma unroll
-          for (int k = 0; k < K; ++k) update(float(k), acc[k]);
+          for (int k = 0; k < H; ++k)
+            update2(__ffma2_rn(make_float2(float(k), float(k)), dv2, v02), acc[k]);
         } else {
+          const float2 v00 = make_float2(v0, v0);
 #pragma unroll
-          for (int k = 0; k < K; ++k) update(float(min(k, kmax)), acc[k]);
+          for (int k = 0; k < H; ++k)
+            update2(__ffma2_rn(make_float2(float(min(k, kmax)), float(min(k + H, kmax))), dv2, v00),
+                    acc[k]);
         }
       } else {
         // general calibrated matrices: full projective map per voxel
@@ -327,7 +346,7 @@ __global__ void __launch_bounds__(NTHREADS, (K <= 16 ? 3 : 2))
           lds_quad<ROWB>(ad, a0, a1, b0, b1);
           const float top = fmaf(wu, a1 - a0, a0);
           const float bot = fmaf(wu, b1 - b0, b0);
-          acc[k] = fmaf(fmaf(wv, bot - top, top), a.sid2 * r * r, acc[k]);
+          ACC(k) = fmaf(fmaf(wv, bot - top, top), a.sid2 * r * r, ACC(k));
         }
       }
     } else if (mode == MODE_SLOW) {
@@ -340,7 +359,7 @@ __global__ void __launch_bounds__(NTHREADS, (K <= 16 ? 3 : 2))
         if (!(hz > 0.0f)) continue;  // behind the source (projector.hpp:302)
         const float u = fmaf(U.z, dz, un) / hz, v = fmaf(V.z, dz, vn) / hz;
         if (!(fabsf(u) < 4.0e6f) || !(fabsf(v) < 4.0e6f)) continue;
-        acc[k] += bilinear_global(a, img, u, v) * (a.sid2 / (hz * hz));
+        ACC(k) += bilinear_global(a, img, u, v) * (a.sid2 / (hz * hz));
       }
     }
     __syncwarp();
@@ -352,7 +371,7 @@ __global__ void __launch_bounds__(NTHREADS, (K <= 16 ? 3 : 2))
   for (int k = 0; k < K; ++k) {
     if (k > kmax) break;
     float* o = a.vol + ((long long)(tile.z0 + k) * a.ny + iy) * a.nx + ix;
-    const float val = acc[k] * a.scale;
+    const float val = ACC(k) * a.scale;
     *o = a.accumulate ? *o + val : val;
   }
 }
@@ -697,6 +716,7 @@ void backproject_impl(tg_cone_plan& p, uint64_t z0, uint64_t nz, uint64_t v0, ui
   a.band_rows = int(n_rows);
   a.boxU = p.boxU;
   a.boxV = p.boxV;
+  a.magic_row_off = 0u - 0x4B400000u * uint32_t(p.boxU * 4);
   a.sino = src;
   a.row_pitch = (long long)pitch;
   a.view_pitch = (long long)(pitch * n_rows);

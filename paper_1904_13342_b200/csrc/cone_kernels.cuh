@@ -39,6 +39,9 @@ struct BpArgs {
   float sid2;               // SID^2: 1/w^2 = SID^2 / hz^2
   float scale;
   int accumulate;
+  // -(0x4B400000 * 4 * BOXU) mod 2^32: the magic-floor bias of a row address,
+  // passed at run time so ptxas cannot split it back out of the per-view base
+  uint32_t magic_row_off;
   const float* sino;        // band buffer (slow path gathers)
   long long row_pitch;      // elements between detector rows
   long long view_pitch;     // elements between views
