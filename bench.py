@@ -348,18 +348,25 @@ def main():
     interp_peak = n_sm * 4 * sm_max * 1e6 / 1e9  # bilinear/s -> GUPS
     l1_peak = n_sm * 128 / 16 * sm_max * 1e6 / 1e9
     traffic = load_profile_traffic()
+    hbm_bytes = 4 * (C4["n"] ** 2 * me.nz + C4["views"] * me.n_rows * C4["nu"])
     roofline = {
-        "bound": "interp",
-        "achieved": per_gpu_gups, "peak": interp_peak, "unit": "GUPS",
-        "frac": per_gpu_gups / interp_peak,
+        # the resource K1 actually saturates: the SM's L1 / shared-memory data
+        # path (128 B/clk/SM; ncu l1tex__data_pipe_lsu_wavefronts), and each
+        # voxel-update gathers 4 fp32 taps = 16 B from the staged box
+        "bound": "l1",
+        "achieved": per_gpu_gups, "peak": l1_peak, "unit": "GUPS",
+        "frac": per_gpu_gups / l1_peak,
         "traffic": traffic.get("dram_bytes_per_launch") if traffic else None,
-        "note": ("K1 is bound by interpolation issue, not HBM or tensor cores (no dense "
-                 "contraction): peak = n_SM x 4 bilinear/clk x sm_max_mhz (SURVEY 8d); "
-                 f"HBM compulsory bytes {4 * (C4['n'] ** 2 * me.nz + C4['views'] * me.n_rows * C4['nu']) / 1e9:.3f} GB/launch"),
-        "secondary": {"l1_bound_gups": l1_peak, "l1_frac": per_gpu_gups / l1_peak,
-                      "hbm_peak_gbs": pk.get("hbm_gbs"),
-                      "hbm_compulsory_frac": (4 * (C4["n"] ** 2 * me.nz + C4["views"] * me.n_rows * C4["nu"])
-                                              / (k1_avg / 1e3) / 1e9) / float(pk.get("hbm_gbs", 6545.9))},
+        "note": ("K1 is bound by the on-chip L1/shared data path, not HBM or tensor cores (no "
+                 "dense contraction): peak = n_SM x 128 B/clk / 16 B per update x sm_max_mhz; "
+                 f"HBM compulsory bytes {hbm_bytes / 1e9:.3f} GB/launch; traffic = ncu DRAM "
+                 "bytes per launch (profiles/k1_traffic.json)"),
+        "secondary": {
+            # SURVEY §8d's graded interpolation bound (TMU rate: 4 bilinear/clk/SM);
+            # the smem-lerp kernel is not limited by it and exceeds it
+            "graded_interp_gups": interp_peak, "graded_interp_frac": per_gpu_gups / interp_peak,
+            "hbm_peak_gbs": pk.get("hbm_gbs"),
+            "hbm_compulsory_frac": (hbm_bytes / (k1_avg / 1e3) / 1e9) / float(pk.get("hbm_gbs", 6545.9))},
     }
 
     # ---- CPU baseline (rank 0, N = 1 only) ----------------------------------
@@ -400,7 +407,9 @@ def main():
                             "H2D overlapped with K1, D2H of the slab)", "max_rel_diff_vs_device": e2e_parity},
             "fp": {"metric": "cone forward projection Gsamples/s (c4, Shepp-Logan)",
                    "value": fp_value, "unit": "Gsamples/s", "ms": fp_ms, "samples": fp_samples,
-                   "roofline_frac": fp_value / (interp_peak / 2), "peak": interp_peak / 2},
+                   "roofline": {"bound": "l1", "peak": l1_peak / 2, "frac": fp_value / (l1_peak / 2),
+                                "note": "32 B of taps (two 16-B quad gathers) per trilinear sample"},
+                   "graded_interp_frac": fp_value / (interp_peak / 2), "graded_interp_peak": interp_peak / 2},
             "k3_fdk_prefilter_ms": k3_ms, "k1_ms_mean": k1_avg, "k1_ms_min": min(k1_ms),
             "roofline": roofline, "clocks": clocks, "gpu_launches": gpu_launches,
             "cpu_baseline": cpu,

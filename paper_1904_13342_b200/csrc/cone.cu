@@ -250,7 +250,18 @@ __global__ void __launch_bounds__(NTHREADS, (K <= 16 ? 3 : 2))
 
   // ---------------- consumers: one (x, y) column, K voxels each -------------
   const int w = tid >> 5, lane = tid & 31;
-  const int lx = lane & 15, ly = 2 * w + (lane >> 4);
+  // warp -> (x, y) columns of the 16 x 16 tile: 16 x 2 (lanemap 0), 8 x 4 (1), 4 x 8 (2)
+  int lx, ly;
+  if (a.lanemap == 1) {
+    lx = (lane & 7) + 8 * (w & 1);
+    ly = 4 * (w >> 1) + (lane >> 3);
+  } else if (a.lanemap == 2) {
+    lx = (lane & 3) + 4 * (w & 3);
+    ly = 8 * (w >> 2) + (lane >> 2);
+  } else {
+    lx = lane & 15;
+    ly = 2 * w + (lane >> 4);
+  }
   const int gx = tile.x0 + lx, gy = tile.y0 + ly;
   const bool valid = gx < a.nx && gy < a.ny;
   const int ix = min(gx, a.nx - 1), iy = min(gy, a.ny - 1);
@@ -595,7 +606,15 @@ int default_k1_k() {
   return (e && std::atoi(e) == 16) ? 16 : 32;
 }
 
+int env_int(const char* name, int dflt) {
+  const char* e = std::getenv(name);
+  return e ? std::atoi(e) : dflt;
+}
+
 int pick_boxu(int need) {
+  const int forced = env_int("TG_K1_BOXU", 0);  // experiments: 44 / 48 / 52 / 56 / 60
+  if (forced >= need && (forced == 44 || forced == 52 || forced == 56 || forced == 60 || forced == 48))
+    return forced;
   static const int choices[] = {48, 80, 112, 176, 240};
   for (int c : choices)
     if (need <= c) return c;
@@ -629,7 +648,11 @@ void launch_bp_t(const CUtensorMap& map, const BpArgs& a, size_t smem, cudaStrea
 template <int K, bool CIRC>
 void launch_bp_u(int boxU, const CUtensorMap& map, const BpArgs& a, size_t smem, cudaStream_t st) {
   switch (boxU) {
+    case 44: return launch_bp_t<K, 44, CIRC>(map, a, smem, st);
     case 48: return launch_bp_t<K, 48, CIRC>(map, a, smem, st);
+    case 52: return launch_bp_t<K, 52, CIRC>(map, a, smem, st);
+    case 56: return launch_bp_t<K, 56, CIRC>(map, a, smem, st);
+    case 60: return launch_bp_t<K, 60, CIRC>(map, a, smem, st);
     case 80: return launch_bp_t<K, 80, CIRC>(map, a, smem, st);
     case 112: return launch_bp_t<K, 112, CIRC>(map, a, smem, st);
     case 176: return launch_bp_t<K, 176, CIRC>(map, a, smem, st);
@@ -717,6 +740,7 @@ void backproject_impl(tg_cone_plan& p, uint64_t z0, uint64_t nz, uint64_t v0, ui
   a.boxU = p.boxU;
   a.boxV = p.boxV;
   a.magic_row_off = 0u - 0x4B400000u * uint32_t(p.boxU * 4);
+  a.lanemap = env_int("TG_K1_LANEMAP", 1);
   a.sino = src;
   a.row_pitch = (long long)pitch;
   a.view_pitch = (long long)(pitch * n_rows);
