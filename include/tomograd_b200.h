@@ -135,6 +135,9 @@ typedef struct tg_cone_plan tg_cone_plan;
 
 tg_status tg_cone_plan_create(const tg_cone_geometry* g, int device, tg_cone_plan** out);
 tg_status tg_cone_plan_destroy(tg_cone_plan* plan);
+/* the plan's volume, detector and view count */
+tg_status tg_cone_plan_shape(const tg_cone_plan* plan, tg_volume_spec* vol, tg_detector2d* det,
+                             uint64_t* n_proj);
 
 /* projector.hpp:264-281 forward_project(Image, ConeGeometry):
  * d_vol [nz][ny][nx] -> d_sino [n_proj][n_v][n_u] */
@@ -193,6 +196,8 @@ typedef struct tg_planar_plan tg_planar_plan;
 
 tg_status tg_planar_plan_create(const tg_planar_geometry* g, int device, tg_planar_plan** out);
 tg_status tg_planar_plan_destroy(tg_planar_plan* plan);
+tg_status tg_planar_plan_shape(const tg_planar_plan* plan, tg_volume_spec* vol,
+                               tg_detector1d* det, uint64_t* n_proj);
 /* projector.hpp:171-184 (parallel) / 212-230 (fan) forward_project */
 tg_status tg_planar_forward(tg_planar_plan* plan, const float* d_img, float* d_sino, void* stream);
 /* projector.hpp:186-208 (parallel) / 232-260 (fan, 1/U^2) back_project */
@@ -227,6 +232,40 @@ tg_status tg_apply_weights(const float* d_in, float* d_out, uint64_t n_total, co
  * Parker map, filtering.hpp:246-247): data [n_views][n_rows][n], map [n_views][n] */
 tg_status tg_apply_row_weights(const float* d_in, float* d_out, uint64_t n_views, uint64_t n_rows,
                                uint64_t n, const double* d_map, void* stream);
+
+/* ---- iterative reconstruction ------------------------
+ * The reference's graph pieces on the device path (graph.hpp, pipelines.hpp:273-299).
+ * Reductions are FP64 with a fixed grid and ordered passes: deterministic. */
+
+/* graph.hpp:345-353 l2_loss value + graph.hpp:498-509 gradient (upstream 1):
+ * d_grad = 2 (a - b) (may alias d_a; NULL = value only); *d_sum = sum (a - b)^2 */
+tg_status tg_l2_residual(const float* d_a, const float* d_b, float* d_grad, uint64_t n,
+                         double* d_sum, void* stream);
+/* graph.hpp:365-377 tv_value, graph.hpp:511-528 subgradient, graph.hpp:533-546
+ * descent, fused: over a [nz][ny][nx] block (x fastest; nz = 1 for images),
+ * x_out = x - lr * (lambda * subgrad_TV(x) + grad), *d_tv = TV of the forward
+ * pairs the block owns.  has_lo / has_hi: the slice before / after the block
+ * exists in memory (a z-slab of a full replica; multi-GPU).  d_grad = d_x_out =
+ * NULL: value only.  d_x_out must not alias d_x. */
+tg_status tg_tv_step(const float* d_x, const float* d_grad, float* d_x_out, uint64_t nx,
+                     uint64_t ny, uint64_t nz, int has_lo, int has_hi, double tv_lambda,
+                     double learning_rate, double* d_tv, void* stream);
+/* pipelines.hpp:273-299 tv_reconstruct (graph: x -> forward_project -> l2_loss(., p)
+ * + tv_lambda * tv_loss(x), plain gradient descent), on any geometry, device
+ * resident: d_x holds the initial image (the reference starts from zero) and
+ * receives the result; h_loss_history[iterations + 1] the loss before every
+ * step and after the last (NULL allowed).  Non-finite loss -> TG_ERROR with the
+ * reference's check_converging message (pipelines.hpp:166-170). */
+tg_status tg_cone_tv_reconstruct(tg_cone_plan* plan, const float* d_sino, float* d_x,
+                                 uint64_t iterations, double learning_rate, double tv_lambda,
+                                 double* h_loss_history, void* stream);
+tg_status tg_planar_tv_reconstruct(tg_planar_plan* plan, const float* d_sino, float* d_x,
+                                   uint64_t iterations, double learning_rate, double tv_lambda,
+                                   double* h_loss_history, void* stream);
+/* pipelines.hpp:119-132 add_gaussian_noise (host, bit-exact: std::mt19937_64
+ * Box-Muller of pipelines.hpp:90-115; sigma = relative_std * max(in)) */
+tg_status tg_add_gaussian_noise(const float* h_in, float* h_out, uint64_t n, double relative_std,
+                                uint64_t seed);
 
 /* ---- synthetic inputs (phantom.hpp:34-88, bit-exact, FP64) ------------- */
 

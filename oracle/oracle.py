@@ -614,6 +614,41 @@ class Ref:
         return out
 
 
+    @staticmethod
+    def tv_reconstruct_planar(g: Planar, sino, iterations, lr, lam):
+        """pipelines.hpp:273-299 (parallel: the reference function itself; fan:
+        the same graph over FanGeometry).  float64 storage (Tensor<double>)."""
+        sino = np.ascontiguousarray(sino, dtype=np.float64)
+        x = np.zeros(g.img_shape_yx)
+        hist = np.zeros(int(iterations) + 1)
+        s = g.struct()
+        fn = ref().ref_tv_reconstruct_fan if g.fan else ref().ref_tv_reconstruct_parallel
+        Ref._chk(fn(C.byref(s), _ptr(sino), _ptr(x), C.c_uint64(int(iterations)),
+                    C.c_double(lr), C.c_double(lam), _ptr(hist)))
+        return x, hist
+
+    @staticmethod
+    def tv_reconstruct_cone(g: Cone, sino, iterations, lr, lam):
+        sino = np.ascontiguousarray(sino, dtype=np.float64)
+        x = np.zeros(g.vol_shape_zyx)
+        hist = np.zeros(int(iterations) + 1)
+        s = g.struct()
+        Ref._chk(ref().ref_tv_reconstruct_cone(C.byref(s), int(g.circular), _ptr(sino), _ptr(x),
+                                               C.c_uint64(int(iterations)), C.c_double(lr),
+                                               C.c_double(lam), _ptr(hist)))
+        return x, hist
+
+    @staticmethod
+    def add_gaussian_noise(data, rel, seed):
+        suf, ct = _typed(data.dtype)
+        data = np.ascontiguousarray(data)
+        out = np.empty_like(data)
+        Ref._chk(getattr(ref(), f"ref_add_gaussian_noise_{suf}")(
+            _ptr(data, ct), _ptr(out, ct), C.c_uint64(data.size), C.c_double(rel),
+            C.c_uint64(int(seed))))
+        return out
+
+
 def rel_errors(out: np.ndarray, ref_: np.ndarray):
     """(max|d| / max|ref|, relRMSE = ||d||2 / ||ref||2) — SURVEY §8c metrics."""
     d = out.astype(np.float64) - ref_.astype(np.float64)
@@ -624,3 +659,79 @@ def rel_errors(out: np.ndarray, ref_: np.ndarray):
 
 
 PI = math.pi
+
+
+# --------------------------------------------------------------------------
+# iterative reconstruction pieces (restatement; graph.hpp / pipelines.hpp)
+
+
+def l2_value(a, b) -> float:
+    suf, ct = _typed(a.dtype)
+    a = np.ascontiguousarray(a); b = np.ascontiguousarray(b, dtype=a.dtype)
+    fn = getattr(lib(), f"or_l2_value_{suf}")
+    fn.restype = C.c_double
+    return float(fn(_ptr(a, ct), _ptr(b, ct), C.c_uint64(a.size)))
+
+
+def _shape_fastest_first(x):
+    return np.array(list(reversed(x.shape)), dtype=np.uint64)
+
+
+def tv_value(x) -> float:
+    suf, ct = _typed(x.dtype)
+    x = np.ascontiguousarray(x)
+    shp = _shape_fastest_first(x)
+    fn = getattr(lib(), f"or_tv_value_{suf}")
+    fn.restype = C.c_double
+    return float(fn(_ptr(x, ct), _ptr(shp, C.c_uint64), C.c_uint32(len(shp))))
+
+
+def tv_subgrad(x, gs=1.0) -> np.ndarray:
+    """graph.hpp:511-528 into a zero gradient (FP64)"""
+    suf, ct = _typed(x.dtype)
+    x = np.ascontiguousarray(x)
+    shp = _shape_fastest_first(x)
+    gx = np.zeros(x.shape)
+    getattr(lib(), f"or_tv_subgrad_acc_{suf}")(_ptr(x, ct), _ptr(shp, C.c_uint64),
+                                                C.c_uint32(len(shp)), C.c_double(gs), _ptr(gx))
+    return gx
+
+
+def tv_reconstruct_planar(g: Planar, sino, iterations, lr, lam):
+    suf, ct = _typed(sino.dtype)
+    sino = np.ascontiguousarray(sino)
+    x = np.zeros(g.img_shape_yx, dtype=sino.dtype)
+    hist = np.zeros(int(iterations) + 1)
+    s = g.struct()
+    _check(getattr(lib(), f"or_tv_reconstruct_planar_{suf}")(
+        C.byref(s), _ptr(sino, ct), _ptr(x, ct), C.c_uint64(int(iterations)), C.c_double(lr),
+        C.c_double(lam), _ptr(hist)))
+    return x, hist
+
+
+def tv_reconstruct_cone(g: Cone, sino, iterations, lr, lam):
+    suf, ct = _typed(sino.dtype)
+    sino = np.ascontiguousarray(sino)
+    x = np.zeros(g.vol_shape_zyx, dtype=sino.dtype)
+    hist = np.zeros(int(iterations) + 1)
+    s = g.struct()
+    _check(getattr(lib(), f"or_tv_reconstruct_cone_{suf}")(
+        C.byref(s), _ptr(sino, ct), _ptr(x, ct), C.c_uint64(int(iterations)), C.c_double(lr),
+        C.c_double(lam), _ptr(hist)))
+    return x, hist
+
+
+def add_gaussian_noise(data, rel, seed):
+    suf, ct = _typed(data.dtype)
+    data = np.ascontiguousarray(data)
+    out = np.empty_like(data)
+    _check(getattr(lib(), f"or_add_gaussian_noise_{suf}")(
+        _ptr(data, ct), _ptr(out, ct), C.c_uint64(data.size), C.c_double(rel),
+        C.c_uint64(int(seed))))
+    return out
+
+
+def mt19937_64(seed, k) -> int:
+    fn = lib().or_mt19937_64_first
+    fn.restype = C.c_uint64
+    return int(fn(C.c_uint64(int(seed)), C.c_uint64(int(k))))

@@ -15,6 +15,7 @@
 #include "tg_oracle.h"
 #include "tomograd/filtering.hpp"
 #include "tomograd/geometry.hpp"
+#include "tomograd/graph.hpp"
 #include "tomograd/image.hpp"
 #include "tomograd/phantom.hpp"
 #include "tomograd/pipelines.hpp"
@@ -81,9 +82,112 @@ Image<T> make_image(const VolumeSpec& s, const T* data) {
   return img;
 }
 
+// pipelines.hpp:276-298 tv_reconstruct, instantiated for any geometry through
+// the reference's own Graph (its nodes take every geometry type,
+// graph.hpp:117-135); for ParallelGeometry the reference function itself is
+// called (ref_tv_reconstruct_parallel).
+template <typename Geo>
+std::vector<double> tv_graph(const Sinogram<>& sino, const Geo& geo, const ExperimentConfig& cfg,
+                             std::vector<double>& x_out) {
+  Graph g;
+  const NodeId x = g.parameter(Tensor<>(geo.volume.shape), /*trainable=*/true);
+  const NodeId p = g.input(sino.shape());
+  const NodeId fp = g.forward_project(x, geo);
+  const NodeId data_term = g.l2_loss(fp, p);
+  const NodeId loss = g.add(data_term, g.scale(g.tv_loss(x), cfg.tv_lambda));
+  std::vector<double> history;
+  const std::map<NodeId, Tensor<>> feeds{{p, sino.tensor()}};
+  for (std::size_t it = 0; it < cfg.iterations; ++it) {
+    g.forward(feeds);
+    history.push_back(g.value(loss).scalar_value());
+    check_converging(history.back(), it);
+    const auto grads = g.backward(loss);
+    gradient_descent_step(g, grads, cfg.learning_rate);
+  }
+  g.forward(feeds);
+  history.push_back(g.value(loss).scalar_value());
+  check_converging(history.back(), cfg.iterations);
+  x_out = g.node(x).value.data;
+  return history;
+}
+
 }  // namespace
 
 extern "C" {
+
+int ref_tv_reconstruct_parallel(const or_planar* g, const double* sino, double* x,
+                                uint64_t iterations, double lr, double lambda, double* hist) {
+  return guard([&] {
+    const auto geo = to_parallel(*g);
+    auto s = Sinogram<>::planar(geo.n_projections, geo.detector);
+    std::memcpy(s.data.data(), sino, sizeof(double) * s.data.size());
+    ExperimentConfig cfg;
+    cfg.learning_rate = lr;
+    cfg.iterations = std::size_t(iterations);
+    cfg.tv_lambda = lambda;
+    auto [rec, h] = tv_reconstruct(s, geo, cfg);
+    std::memcpy(x, rec.data.data(), sizeof(double) * rec.data.size());
+    std::memcpy(hist, h.data(), sizeof(double) * h.size());
+  });
+}
+
+int ref_tv_reconstruct_fan(const or_planar* g, const double* sino, double* x, uint64_t iterations,
+                           double lr, double lambda, double* hist) {
+  return guard([&] {
+    const auto geo = to_fan(*g);
+    auto s = Sinogram<>::planar(geo.n_projections, geo.detector);
+    std::memcpy(s.data.data(), sino, sizeof(double) * s.data.size());
+    ExperimentConfig cfg;
+    cfg.learning_rate = lr;
+    cfg.iterations = std::size_t(iterations);
+    cfg.tv_lambda = lambda;
+    std::vector<double> xv;
+    auto h = tv_graph(s, geo, cfg, xv);
+    std::memcpy(x, xv.data(), sizeof(double) * xv.size());
+    std::memcpy(hist, h.data(), sizeof(double) * h.size());
+  });
+}
+
+int ref_tv_reconstruct_cone(const or_cone* g, int circular, const double* sino, double* x,
+                            uint64_t iterations, double lr, double lambda, double* hist) {
+  return guard([&] {
+    const auto geo = to_cone(*g, circular != 0);
+    auto s = Sinogram<>::cone_beam(geo.n_projections, geo.detector);
+    std::memcpy(s.data.data(), sino, sizeof(double) * s.data.size());
+    ExperimentConfig cfg;
+    cfg.learning_rate = lr;
+    cfg.iterations = std::size_t(iterations);
+    cfg.tv_lambda = lambda;
+    std::vector<double> xv;
+    auto h = tv_graph(s, geo, cfg, xv);
+    std::memcpy(x, xv.data(), sizeof(double) * xv.size());
+    std::memcpy(hist, h.data(), sizeof(double) * h.size());
+  });
+}
+
+// pipelines.hpp:119-132 on a planar sinogram of n values (the stream depends
+// only on the flat data order)
+int ref_add_gaussian_noise_f64(const double* in, double* out, uint64_t n, double rel,
+                               uint64_t seed) {
+  return guard([&] {
+    Detector1D d{std::size_t(n), 1.0, 0.0};
+    auto s = Sinogram<double>::planar(1, d);
+    std::memcpy(s.data.data(), in, sizeof(double) * n);
+    auto o = add_gaussian_noise(s, rel, seed);
+    std::memcpy(out, o.data.data(), sizeof(double) * n);
+  });
+}
+
+int ref_add_gaussian_noise_f32(const float* in, float* out, uint64_t n, double rel, uint64_t seed) {
+  return guard([&] {
+    Detector1D d{std::size_t(n), 1.0, 0.0};
+    auto s = Sinogram<float>::planar(1, d);
+    std::memcpy(s.data.data(), in, sizeof(float) * n);
+    auto o = add_gaussian_noise(s, rel, seed);
+    std::memcpy(out, o.data.data(), sizeof(float) * n);
+  });
+}
+
 
 const char* ref_last_error(void) { return g_err.c_str(); }
 void ref_set_threads(int n) { set_num_threads(unsigned(n < 1 ? 1 : n)); }

@@ -461,6 +461,70 @@ double or_fov_half_extent(const or_volume* vol) {
   return 0.5 * h;
 }
 
+/* ---- pipelines.hpp:90-115 GaussianSource: std::mt19937_64 + Box-Muller --- */
+
+/* std::mt19937_64 (the C++ standard's parameters: w=64, n=312, m=156, r=31,
+ * a=0xB5026F5AA96619E9, u=29, d=0x5555555555555555, s=17, b=0x71D67FFFEDA60000,
+ * t=37, c=0xFFF7EEE000000000, l=43, f=6364136223846793005) */
+typedef struct {
+  uint64_t mt[312];
+  int idx;
+} or_mt64;
+
+static void mt64_seed(or_mt64* g, uint64_t seed) {
+  g->mt[0] = seed;
+  for (int i = 1; i < 312; ++i)
+    g->mt[i] = 6364136223846793005ULL * (g->mt[i - 1] ^ (g->mt[i - 1] >> 62)) + (uint64_t)i;
+  g->idx = 312;
+}
+
+static uint64_t mt64_next(or_mt64* g) {
+  if (g->idx >= 312) {
+    const uint64_t UM = 0xFFFFFFFF80000000ULL, LM = 0x7FFFFFFFULL;
+    for (int i = 0; i < 312; ++i) {
+      const uint64_t x = (g->mt[i] & UM) | (g->mt[(i + 1) % 312] & LM);
+      uint64_t xa = x >> 1;
+      if (x & 1ULL) xa ^= 0xB5026F5AA96619E9ULL;
+      g->mt[i] = g->mt[(i + 156) % 312] ^ xa;
+    }
+    g->idx = 0;
+  }
+  uint64_t y = g->mt[g->idx++];
+  y ^= (y >> 29) & 0x5555555555555555ULL;
+  y ^= (y << 17) & 0x71D67FFFEDA60000ULL;
+  y ^= (y << 37) & 0xFFF7EEE000000000ULL;
+  y ^= y >> 43;
+  return y;
+}
+
+typedef struct {
+  or_mt64 rng;
+  int have;
+  double cached;
+} or_gauss;
+
+static double gauss_next(or_gauss* g) {
+  if (g->have) {
+    g->have = 0;
+    return g->cached;
+  }
+  const double u1 = ((double)(mt64_next(&g->rng) >> 11) + 1.0) * 0x1.0p-53; /* (0, 1] */
+  const double u2 = (double)(mt64_next(&g->rng) >> 11) * 0x1.0p-53;         /* [0, 1) */
+  const double r = sqrt(-2.0 * log(u1));
+  const double a = 2.0 * OR_PI * u2;
+  g->cached = r * sin(a);
+  g->have = 1;
+  return r * cos(a);
+}
+
+uint64_t or_mt19937_64_first(uint64_t seed, uint64_t k) {
+  or_mt64 g;
+  mt64_seed(&g, seed);
+  uint64_t v = 0;
+  for (uint64_t i = 0; i < k; ++i) v = mt64_next(&g);
+  return v;
+}
+
 /* ---- storage-typed operators (instantiated for float and double) ------- */
 
 #define T float

@@ -104,6 +104,23 @@ int or_make_cone(const or_det2* det, uint64_t n, double range, double sid, doubl
                                     T* out);                                                \
   int or_rasterize_ellipses_##SUF(const or_volume* vol, const double* specs, uint64_t n,   \
                                   T* out);
+#define OR_DECLARE_ITER(SUF, T)                                                             \
+  double or_l2_value_##SUF(const T* a, const T* b, uint64_t n);                             \
+  double or_tv_value_##SUF(const T* x, const uint64_t* shape, uint32_t dims);               \
+  void or_tv_subgrad_acc_##SUF(const T* x, const uint64_t* shape, uint32_t dims, double gs,  \
+                               double* gx);                                                  \
+  int or_tv_reconstruct_cone_##SUF(const or_cone* g, const T* sino, T* x, uint64_t iters,    \
+                                   double lr, double lambda, double* hist);                  \
+  int or_tv_reconstruct_planar_##SUF(const or_planar* g, const T* sino, T* x,              \
+                                     uint64_t iters, double lr, double lambda, double* hist); \
+  int or_add_gaussian_noise_##SUF(const T* in, T* out, uint64_t n, double relative_std,     \
+                                  uint64_t seed);
+OR_DECLARE_ITER(f32, float)
+OR_DECLARE_ITER(f64, double)
+#undef OR_DECLARE_ITER
+/* k-th output (1-based) of std::mt19937_64(seed) */
+uint64_t or_mt19937_64_first(uint64_t seed, uint64_t k);
+
 OR_DECLARE(f32, float)
 OR_DECLARE(f64, double)
 #undef OR_DECLARE

@@ -17,6 +17,8 @@ from .geometry import (ConeGeometry, Detector1D, Detector2D, FanGeometry,  # noq
                        projection_matrices_circular, view_angles)
 from .phantom import (disk_phantom, head_phantom_ellipses, head_phantom_ellipsoids,  # noqa: F401
                       rasterize, shepp_logan_2d, shepp_logan_3d)
+from .iterative import (ExperimentConfig, TvResult, add_gaussian_noise,  # noqa: F401
+                        experiment_iterative_tv, l2_residual, tv_reconstruct, tv_step)
 from .pipelines import (FilterKind, fbp_reconstruct, fdk_prefilter, fdk_reconstruct,  # noqa: F401
                         fdk_scale, make_filter)
 from .projector import (back_project, cone_backproject_slab, cone_forward_views,  # noqa: F401

@@ -100,6 +100,14 @@ SIGNATURES = {
     "tg_rasterize_ellipses": (c_int, [_P(tg_volume_spec), c_dblp, c_u64, c_vp, c_vp]),
     "tg_head_phantom_ellipsoids": (c_int, [_P(tg_volume_spec), c_dblp]),
     "tg_head_phantom_ellipses": (c_int, [_P(tg_volume_spec), c_dblp]),
+    "tg_cone_plan_shape": (c_int, [c_vp, _P(tg_volume_spec), _P(tg_detector2d), c_u64p]),
+    "tg_planar_plan_shape": (c_int, [c_vp, _P(tg_volume_spec), _P(tg_detector1d), c_u64p]),
+    "tg_l2_residual": (c_int, [c_vp, c_vp, c_vp, c_u64, c_vp, c_vp]),
+    "tg_tv_step": (c_int, [c_vp, c_vp, c_vp, c_u64, c_u64, c_u64, c_int, c_int, c_dbl, c_dbl, c_vp,
+                           c_vp]),
+    "tg_cone_tv_reconstruct": (c_int, [c_vp, c_vp, c_vp, c_u64, c_dbl, c_dbl, c_dblp, c_vp]),
+    "tg_planar_tv_reconstruct": (c_int, [c_vp, c_vp, c_vp, c_u64, c_dbl, c_dbl, c_dblp, c_vp]),
+    "tg_add_gaussian_noise": (c_int, [c_vp, c_vp, c_u64, c_dbl, c_u64]),
     "tg_kernel_launch_count": (c_u64, []),
     "tg_set_timing": (None, [c_int]),
     "tg_last_kernel_ms": (c_dbl, []),

@@ -1036,6 +1036,16 @@ tg_status tg_cone_plan_destroy(tg_cone_plan* p) {
   });
 }
 
+tg_status tg_cone_plan_shape(const tg_cone_plan* p, tg_volume_spec* vol, tg_detector2d* det,
+                             uint64_t* n_proj) {
+  return guarded([&] {
+    check(p != nullptr, "null plan");
+    if (vol) *vol = p->vol;
+    if (det) *det = p->det;
+    if (n_proj) *n_proj = p->n_proj;
+  });
+}
+
 tg_status tg_cone_forward(tg_cone_plan* p, const float* d_vol, float* d_sino, void* stream) {
   return guarded([&] { forward_impl(*p, 0, p->n_proj, d_vol, d_sino, as_stream(stream)); });
 }

@@ -10,6 +10,7 @@
 #include <complex>
 #include <cstring>
 #include <mutex>
+#include <random>
 #include <string>
 #include <utility>
 #include <vector>
@@ -278,7 +279,52 @@ double fov_half_extent(const tg_volume_spec& v) {  // phantom.hpp:124-128
 
 using namespace tgb;
 
+namespace tgb {
+namespace {
+// pipelines.hpp:90-115 GaussianSource: Box-Muller on explicit mt19937_64 draws
+class GaussianSource {
+ public:
+  explicit GaussianSource(uint64_t seed) : rng_(seed) {}
+  double next() {
+    if (have_) {
+      have_ = false;
+      return cached_;
+    }
+    const double u1 = (double(rng_() >> 11) + 1.0) * 0x1.0p-53;  // (0, 1]
+    const double u2 = double(rng_() >> 11) * 0x1.0p-53;          // [0, 1)
+    const double r = std::sqrt(-2.0 * std::log(u1));
+    const double a = 2.0 * kPi * u2;
+    cached_ = r * std::sin(a);
+    have_ = true;
+    return r * std::cos(a);
+  }
+
+ private:
+  std::mt19937_64 rng_;
+  bool have_ = false;
+  double cached_ = 0.0;
+};
+}  // namespace
+}  // namespace tgb
+
 extern "C" {
+
+tg_status tg_add_gaussian_noise(const float* in, float* out, uint64_t n, double relative_std,
+                                uint64_t seed) {
+  return tgb::guarded([&] {
+    // pipelines.hpp:119-132
+    tgb::check(relative_std >= 0.0, "noise level must be non-negative");
+    if (relative_std == 0.0) {
+      if (out != in) std::memmove(out, in, n * sizeof(float));
+      return;
+    }
+    double peak = 0.0;
+    for (uint64_t i = 0; i < n; ++i) peak = (peak < double(in[i])) ? double(in[i]) : peak;
+    const double sigma = relative_std * peak;
+    tgb::GaussianSource gauss(seed);
+    for (uint64_t i = 0; i < n; ++i) out[i] = float(double(in[i]) + sigma * gauss.next());
+  });
+}
 
 const char* tg_last_error(void) { return tgb::t_last_error.c_str(); }
 int tg_abi_version(void) { return TG_ABI_VERSION; }

@@ -1,0 +1,272 @@
+// iterative.cu — the TV-regularised iterative reconstruction loop (SURVEY §8f
+// row 1): the reference's graph pieces on the device path.
+//
+//   loss(x) = |A x - p|^2 + lambda * TV(x),  x <- x - lr * grad      (pipelines.hpp:273-299)
+//
+// Reference pieces restated here:
+//   l2_loss value / gradient            graph.hpp:345-353, 498-509
+//   tv_loss value (anisotropic, forward differences over every axis)
+//                                        graph.hpp:365-377
+//   tv_loss subgradient (sign, flat -> 0) graph.hpp:511-528
+//   gradient_descent_step               graph.hpp:533-546
+//   check_converging                    pipelines.hpp:166-170
+//
+// K8 l2_residual_kernel: one pass over the sinogram: g = 2 (a - b) in place
+//    and sum (a - b)^2 in FP64 (fixed grid + ordered second pass: bit-for-bit
+//    deterministic run to run).  HBM-bound: 12 B per detector pixel.
+// K9 tv_step_kernel: one pass over the volume (or a z-slab of it with
+//    one-slice halos): TV value of the forward differences it owns, the
+//    subgradient, the data gradient (the back-projection) and the descent
+//    update fused; x is double-buffered.  HBM-bound: 12 B per voxel
+//    (x, grad in; x' out), neighbour re-reads hit L1/L2.
+#include <cmath>
+#include <string>
+#include <vector>
+
+#include "device_common.cuh"
+
+namespace tgb {
+namespace iter {
+
+constexpr int kRedBlocks = 148 * 8;  // fixed reduction grid (deterministic partials)
+constexpr int kRedThreads = 256;
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// block-level sum in a fixed order; result valid in thread 0
+__device__ __forceinline__ double block_sum(double v) {
+  __shared__ double ws[kRedThreads / 32];
+  v = warp_sum(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) ws[w] = v;
+  __syncthreads();
+  double r = 0.0;
+  if (threadIdx.x == 0)
+    for (int i = 0; i < kRedThreads / 32; ++i) r += ws[i];
+  __syncthreads();
+  return r;
+}
+
+// K8: g = 2 * gs * (a - b) (graph.hpp:503: d = 2.0 * gs * (a[i] - b[i])),
+// partial[block] = sum (a - b)^2 (graph.hpp:347-351)
+__global__ void __launch_bounds__(kRedThreads) l2_residual_kernel(const float* a,
+                                                                   const float* __restrict__ b,
+                                                                   float* g, uint64_t n, double gs2,
+                                                                   double* __restrict__ partial) {
+  double acc = 0.0;
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const double d = double(a[i]) - double(b[i]);
+    acc += d * d;
+    if (g) g[i] = float(gs2 * d);
+  }
+  acc = block_sum(acc);
+  if (threadIdx.x == 0) partial[blockIdx.x] = acc;
+}
+
+// ordered sum of kRedBlocks partials -> out[0]
+__global__ void sum_partials_kernel(const double* __restrict__ partial, int n, double* out) {
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) acc += partial[i];
+  acc = block_sum(acc);
+  if (threadIdx.x == 0) out[0] = acc;
+}
+
+__device__ __forceinline__ int sgn(double d) { return (d > 0.0) - (d < 0.0); }
+
+// K9: over the voxels of a slab [nz][ny][nx] (x fastest) whose z neighbours
+// outside the slab exist when has_lo / has_hi (the caller's pointer is into a
+// full replica).  For each voxel i:
+//   s_i = sum_a [ sgn(x_i - x_{i-s_a}) ] - [ sgn(x_{i+s_a} - x_i) ]
+//   x'_i = x_i - lr * (lambda * s_i + grad_i)
+// and the TV of the forward pairs (i, i + s_a) it owns.  Differences of fp32
+// values are exact in FP64, so signs and |d| are exactly the reference's for
+// the same x.  x_out == nullptr: value only.
+__global__ void __launch_bounds__(kRedThreads) tv_step_kernel(
+    const float* __restrict__ x, const float* __restrict__ grad, float* __restrict__ x_out, int nx,
+    int ny, int nz, int has_lo, int has_hi, double lambda, double lr, double* __restrict__ partial) {
+  const long long plane = (long long)nx * ny;
+  const long long n = plane * nz;
+  double tv = 0.0;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const int ix = int(i % nx);
+    const long long r = i / nx;
+    const int iy = int(r % ny), iz = int(r / ny);
+    const double xi = x[i];
+    int s = 0;
+    if (ix >= 1) s += sgn(xi - double(x[i - 1]));
+    if (ix + 1 < nx) {
+      const double d = double(x[i + 1]) - xi;
+      s -= sgn(d);
+      tv += fabs(d);
+    }
+    if (iy >= 1) s += sgn(xi - double(x[i - nx]));
+    if (iy + 1 < ny) {
+      const double d = double(x[i + nx]) - xi;
+      s -= sgn(d);
+      tv += fabs(d);
+    }
+    if (iz >= 1 || has_lo) s += sgn(xi - double(x[i - plane]));
+    if (iz + 1 < nz || has_hi) {
+      const double d = double(x[i + plane]) - xi;
+      s -= sgn(d);
+      tv += fabs(d);
+    }
+    if (x_out) {
+      const double g = lambda * double(s) + double(grad[i]);
+      x_out[i] = float(xi - lr * g);
+    }
+  }
+  tv = block_sum(tv);
+  if (threadIdx.x == 0) partial[blockIdx.x] = tv;
+}
+
+// stream-ordered device buffer (pool-backed: no device-wide sync)
+template <typename T>
+struct AsyncBuf {
+  T* p = nullptr;
+  cudaStream_t st;
+  AsyncBuf(size_t n, cudaStream_t s) : st(s) { TG_CUDA(cudaMallocAsync(&p, n * sizeof(T), st)); }
+  ~AsyncBuf() { cudaFreeAsync(p, st); }
+  AsyncBuf(const AsyncBuf&) = delete;
+  AsyncBuf& operator=(const AsyncBuf&) = delete;
+};
+
+struct Scratch {
+  AsyncBuf<double> buf;
+  double* partial;
+  explicit Scratch(cudaStream_t s) : buf(kRedBlocks, s), partial(buf.p) {}
+};
+
+void l2_residual(const float* a, const float* b, float* g, uint64_t n, double* d_sum,
+                 cudaStream_t st, const Scratch& sc) {
+  l2_residual_kernel<<<kRedBlocks, kRedThreads, 0, st>>>(a, b, g, n, 2.0 * 1.0, sc.partial);
+  sum_partials_kernel<<<1, kRedThreads, 0, st>>>(sc.partial, kRedBlocks, d_sum);
+  TG_LAUNCHED(2);
+}
+
+void tv_step(const float* x, const float* grad, float* x_out, uint64_t nx, uint64_t ny, uint64_t nz,
+             int has_lo, int has_hi, double lambda, double lr, double* d_tv, cudaStream_t st,
+             const Scratch& sc) {
+  tv_step_kernel<<<kRedBlocks, kRedThreads, 0, st>>>(x, grad, x_out, int(nx), int(ny), int(nz),
+                                                      has_lo, has_hi, lambda, lr, sc.partial);
+  sum_partials_kernel<<<1, kRedThreads, 0, st>>>(sc.partial, kRedBlocks, d_tv);
+  TG_LAUNCHED(2);
+}
+
+// One device-resident descent loop over any projector pair (fwd, bwd) —
+// pipelines.hpp:276-298 with the graph's evaluation order: forward (loss of
+// the current x), backward, step; a final forward records the last loss.
+template <typename Fwd, typename Bwd>
+void tv_loop(Fwd fwd, Bwd bwd, uint64_t n_sino, uint64_t nx, uint64_t ny, uint64_t nz,
+             const float* d_sino, float* d_x, uint64_t iterations, double lr, double lambda,
+             double* h_hist, cudaStream_t st) {
+  const uint64_t n_vox = nx * ny * nz;
+  AsyncBuf<float> fp_b(n_sino, st), bp_b(n_vox, st), x2_b(n_vox, st);
+  AsyncBuf<double> sums_b(2 * (iterations + 1), st);  // [iterations + 1][2] = (data, tv)
+  float *fp = fp_b.p, *bp = bp_b.p, *x2 = x2_b.p;
+  double* sums = sums_b.p;
+  Scratch sc(st);
+  float* cur = d_x;
+  float* nxt = x2;
+  for (uint64_t it = 0; it < iterations; ++it) {
+    fwd(cur, fp);
+    l2_residual(fp, d_sino, fp, n_sino, sums + 2 * it, st, sc);
+    bwd(fp, bp);
+    tv_step(cur, bp, nxt, nx, ny, nz, 0, 0, lambda, lr, sums + 2 * it + 1, st, sc);
+    std::swap(cur, nxt);
+  }
+  fwd(cur, fp);
+  l2_residual(fp, d_sino, nullptr, n_sino, sums + 2 * iterations, st, sc);
+  tv_step(cur, nullptr, nullptr, nx, ny, nz, 0, 0, lambda, lr, sums + 2 * iterations + 1, st, sc);
+  if (cur != d_x)
+    TG_CUDA(cudaMemcpyAsync(d_x, cur, n_vox * sizeof(float), cudaMemcpyDeviceToDevice, st));
+  std::vector<double> s(2 * (iterations + 1));
+  TG_CUDA(cudaMemcpyAsync(s.data(), sums, s.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
+  TG_CUDA(cudaStreamSynchronize(st));
+  for (uint64_t it = 0; it <= iterations; ++it) {
+    // graph add node: data + (tv * lambda)   (graph.hpp:331-343)
+    const double loss = s[2 * it] + s[2 * it + 1] * lambda;
+    if (h_hist) h_hist[it] = loss;
+    if (!std::isfinite(loss))
+      throw RefError("optimization diverged at iteration " + std::to_string(it) +
+                     " (loss is not finite); lower the learning rate");
+  }
+}
+
+}  // namespace iter
+}  // namespace tgb
+
+using namespace tgb;
+
+extern "C" {
+
+tg_status tg_l2_residual(const float* d_a, const float* d_b, float* d_grad, uint64_t n,
+                         double* d_sum, void* stream) {
+  return guarded([&] {
+    check(n >= 1, "l2_loss expects matching shapes");
+    const cudaStream_t st = as_stream(stream);
+    iter::Scratch sc(st);
+    iter::l2_residual(d_a, d_b, d_grad, n, d_sum, st, sc);
+  });
+}
+
+tg_status tg_tv_step(const float* d_x, const float* d_grad, float* d_x_out, uint64_t nx,
+                     uint64_t ny, uint64_t nz, int has_lo, int has_hi, double tv_lambda,
+                     double learning_rate, double* d_tv, void* stream) {
+  return guarded([&] {
+    check(nx >= 1 && ny >= 1 && nz >= 1, "tv_loss needs a non-scalar input");
+    check((d_x_out == nullptr) == (d_grad == nullptr), "tv_step: x_out and grad go together");
+    check(d_x_out == nullptr || d_x_out != d_x, "tv_step: x_out must not alias x");
+    const cudaStream_t st = as_stream(stream);
+    iter::Scratch sc(st);
+    iter::tv_step(d_x, d_grad, d_x_out, nx, ny, nz, has_lo != 0, has_hi != 0, tv_lambda,
+                  learning_rate, d_tv, st, sc);
+  });
+}
+
+tg_status tg_cone_tv_reconstruct(tg_cone_plan* plan, const float* d_sino, float* d_x,
+                                 uint64_t iterations, double learning_rate, double tv_lambda,
+                                 double* h_loss_history, void* stream) {
+  return guarded([&] {
+    const cudaStream_t st = as_stream(stream);
+    tg_volume_spec vol;
+    tg_detector2d det;
+    uint64_t n_proj = 0;
+    tg_cone_plan_shape(plan, &vol, &det, &n_proj);
+    auto ok = [](tg_status s) {
+      if (s != TG_OK) throw RefError(tg_last_error());
+    };
+    iter::tv_loop([&](const float* x, float* s) { ok(tg_cone_forward(plan, x, s, st)); },
+                  [&](const float* s, float* x) { ok(tg_cone_backproject(plan, s, x, 1.0f, 0, st)); },
+                  n_proj * det.n_u * det.n_v, vol.shape[0], vol.shape[1], vol.shape[2], d_sino,
+                  d_x, iterations, learning_rate, tv_lambda, h_loss_history, st);
+  });
+}
+
+tg_status tg_planar_tv_reconstruct(tg_planar_plan* plan, const float* d_sino, float* d_x,
+                                   uint64_t iterations, double learning_rate, double tv_lambda,
+                                   double* h_loss_history, void* stream) {
+  return guarded([&] {
+    const cudaStream_t st = as_stream(stream);
+    tg_volume_spec vol;
+    tg_detector1d det;
+    uint64_t n_proj = 0;
+    tg_planar_plan_shape(plan, &vol, &det, &n_proj);
+    auto ok = [](tg_status s) {
+      if (s != TG_OK) throw RefError(tg_last_error());
+    };
+    iter::tv_loop(
+        [&](const float* x, float* s) { ok(tg_planar_forward(plan, x, s, st)); },
+        [&](const float* s, float* x) { ok(tg_planar_backproject(plan, s, x, 1.0f, 0, st)); },
+        n_proj * det.n_bins, vol.shape[0], vol.shape[1], 1, d_sino, d_x, iterations,
+        learning_rate, tv_lambda, h_loss_history, st);
+  });
+}
+
+}  // extern "C"

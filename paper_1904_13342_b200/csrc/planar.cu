@@ -335,6 +335,16 @@ tg_status tg_planar_plan_destroy(tg_planar_plan* p) {
   });
 }
 
+tg_status tg_planar_plan_shape(const tg_planar_plan* p, tg_volume_spec* vol, tg_detector1d* det,
+                               uint64_t* n_proj) {
+  return guarded([&] {
+    check(p != nullptr, "null plan");
+    if (vol) *vol = p->vol;
+    if (det) *det = p->det;
+    if (n_proj) *n_proj = p->n_proj;
+  });
+}
+
 tg_status tg_planar_forward(tg_planar_plan* p, const float* d_img, float* d_sino, void* stream) {
   return guarded([&] { planar_forward_impl(*p, d_img, d_sino, as_stream(stream)); });
 }

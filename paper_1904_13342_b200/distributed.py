@@ -10,11 +10,24 @@
   projects its view range.
 * Collectives (NCCL over NVLink on a B200 box, gloo in the CPU tests) exist
   only to reassemble results between passes of an iterative loop:
-  ``gather_slabs`` (all_gather of z-slabs) and ``gather_views``.
+  ``gather_slabs`` (all_gather of z-slabs), ``gather_views`` and
+  ``exchange_bands`` (all_to_all of residual row bands from angle owners to
+  slab owners).
+* ``tv_reconstruct_sharded`` is the config-5 loop (pipelines.hpp:273-299 on a
+  cone geometry) over that decomposition: per iteration each rank projects
+  its views from its volume replica (K2), forms the l2 residual (K8), sends
+  every slab owner the rows of it that slab needs (one all_to_all), back-
+  projects its own slab from the received band (K1), applies the fused TV
+  subgradient + descent step to its slab with one-slice halos read from the
+  replica (K9), and all_gathers the slabs into the next replica.  The two
+  loss partials travel in one small all_gather and are summed in rank order
+  (bit-identical on every rank).  The image is bitwise independent of the
+  world size (32-aligned slabs, per-view projections, per-voxel updates).
 """
 from __future__ import annotations
 
 import ctypes as C
+import math
 from dataclasses import dataclass
 from typing import List, Tuple
 
@@ -61,8 +74,8 @@ class SlabShard:
     n_rows: int
 
 
-def slab_shards(geo: ConeGeometry, world: int) -> List[SlabShard]:
-    parts = even_partition(geo.volume.shape[2], world, Z_ALIGN)
+def slab_shards(geo: ConeGeometry, world: int, align: int = Z_ALIGN) -> List[SlabShard]:
+    parts = even_partition(geo.volume.shape[2], world, align)
     out = []
     for r, (z0, nz) in enumerate(parts):
         v0, nr = slab_rows(geo, z0, nz) if nz > 0 else (0, 1)
@@ -104,3 +117,130 @@ def gather_views(part: torch.Tensor, parts: List[Tuple[int, int]], group=None) -
     bufs = [torch.empty_like(pad) for _ in parts]
     dist.all_gather(bufs, pad, group=group)
     return torch.cat([b[:c] for b, (_, c) in zip(bufs, parts)], dim=0)
+
+
+# ---------------------------------------------------------------------------
+# collectives over CPU (gloo) or device (NCCL) tensors
+
+
+def _staged(t: torch.Tensor, group=None):
+    """gloo has no device collectives: stage CUDA tensors through the host."""
+    if t.is_cuda and dist.get_backend(group) == "gloo":
+        return t.cpu(), True
+    return t, False
+
+
+def exchange_bands(grad_part: torch.Tensor, view_parts: List[Tuple[int, int]],
+                   shards: List[SlabShard], rank: int, group=None) -> torch.Tensor:
+    """all_to_all: this rank holds the residual of its views
+    ``grad_part`` [n_views_r][n_v][n_u]; every slab owner s receives rows
+    [v0_s, v0_s + n_rows_s) of every view.  Returns this rank's band
+    [n_proj][n_rows][n_u] (views arrive in rank order = view order)."""
+    nu = grad_part.shape[2]
+    me = shards[rank]
+    send = torch.cat([grad_part[:, s.v0:s.v0 + s.n_rows, :].reshape(-1) for s in shards])
+    in_splits = [grad_part.shape[0] * s.n_rows * nu for s in shards]
+    out_splits = [c * me.n_rows * nu for _, c in view_parts]
+    send_t, staged = _staged(send, group)
+    recv = torch.empty(sum(out_splits), dtype=send.dtype, device=send_t.device)
+    dist.all_to_all_single(recv, send_t, out_splits, in_splits, group=group)
+    if staged:
+        recv = recv.to(grad_part.device)
+    n_proj = sum(c for _, c in view_parts)
+    return recv.view(n_proj, me.n_rows, nu)
+
+
+def gather_slabs_into(slab: torch.Tensor, shards: List[SlabShard], out: torch.Tensor,
+                      group=None) -> torch.Tensor:
+    """all_gather z-slabs into the preallocated full volume ``out``."""
+    full = gather_slabs(*_staged(slab, group)[:1], shards, group=group)
+    out.copy_(full)
+    return out
+
+
+def sum_in_rank_order(values: List[float], device, group=None) -> List[float]:
+    """all_gather small FP64 partials and sum them in rank order (the same
+    bits on every rank, independent of the collective's reduction order)."""
+    t = torch.tensor(values, dtype=torch.float64,
+                     device=device if dist.get_backend(group) != "gloo" else "cpu")
+    world = dist.get_world_size(group)
+    bufs = [torch.empty_like(t) for _ in range(world)]
+    dist.all_gather(bufs, t, group=group)
+    tot = [0.0] * len(values)
+    for b in bufs:
+        for i, v in enumerate(b.tolist()):
+            tot[i] += v
+    return tot
+
+
+class CudaTvOps:
+    """The device operations of one rank of the sharded TV loop (the product
+    path: K2, K8, K1, K9 through the C ABI)."""
+
+    def __init__(self, geo: ConeGeometry):
+        self.geo = geo
+
+    def forward_views(self, x, v0, n, out):
+        from .projector import cone_forward_views
+        return cone_forward_views(self.geo, x, v0, n, out=out)
+
+    def residual(self, fp, p, grad):
+        from .iterative import l2_residual
+        return l2_residual(fp, p, grad)
+
+    def backproject_slab(self, band, shard, out):
+        from .projector import cone_backproject_slab
+        return cone_backproject_slab(self.geo, band, shard.z0, shard.nz, shard.v0, out=out,
+                                     scale=1.0)
+
+    def tv_step(self, x, shard, grad, out, lam, lr):
+        from .iterative import tv_step
+        nz_all = x.shape[0]
+        xs = x[shard.z0:shard.z0 + shard.nz]
+        return tv_step(xs, grad, out, lam, lr, has_lo=shard.z0 > 0,
+                       has_hi=shard.z0 + shard.nz < nz_all, x_base=x)
+
+    def zeros(self, shape, like):
+        return torch.zeros(shape, dtype=torch.float32, device=like.device)
+
+
+def tv_reconstruct_sharded(geo: ConeGeometry, p_part: torch.Tensor, iterations: int,
+                           learning_rate: float, tv_lambda: float, group=None, ops=None,
+                           align: int = Z_ALIGN, x0: torch.Tensor = None):
+    """pipelines.hpp:273-299 over world ranks.
+
+    p_part: this rank's views [view_partition(geo, world)[rank]] of the
+    measured sinogram.  Returns (full image replica, loss history
+    [iterations + 1]); raises the reference's divergence Error."""
+    from ._native import Error
+    ops = ops or CudaTvOps(geo)
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    shards = slab_shards(geo, world, align)
+    views = view_partition(geo, world)
+    me = shards[rank]
+    vw0, vwn = views[rank]
+    nx, ny, nz = geo.volume.shape
+    x = ops.zeros((nz, ny, nx), p_part) if x0 is None else x0.clone()
+    fp = ops.zeros((vwn, geo.detector.n_v, geo.detector.n_u), p_part)
+    bp = ops.zeros((me.nz, ny, nx), p_part)
+    xs = ops.zeros((me.nz, ny, nx), p_part)
+    hist = []
+    for it in range(iterations + 1):
+        ops.forward_views(x, vw0, vwn, fp)
+        last = it == iterations
+        data = ops.residual(fp, p_part, None if last else fp)
+        if last:
+            tv = ops.tv_step(x, me, None, None, tv_lambda, learning_rate)
+        else:
+            band = exchange_bands(fp, views, shards, rank, group)
+            ops.backproject_slab(band, me, bp)
+            tv = ops.tv_step(x, me, bp, xs, tv_lambda, learning_rate)
+        d, t = sum_in_rank_order([data, tv], p_part.device, group)
+        loss = d + t * tv_lambda
+        hist.append(loss)
+        if not math.isfinite(loss):
+            raise Error(f"optimization diverged at iteration {it} (loss is not finite); "
+                        "lower the learning rate")
+        if not last:
+            gather_slabs_into(xs, shards, x, group)
+    return x, hist

@@ -1,0 +1,161 @@
+"""Iterative TV-regularised reconstruction on the device
+path: pipelines.hpp:273-312 over the graph pieces of graph.hpp.
+
+    tv_reconstruct(sino, geo, cfg) -> (Image, loss_history)      pipelines.hpp:273-299
+    experiment_iterative_tv(geo, cfg) -> TvResult                pipelines.hpp:301-312
+    add_gaussian_noise(sino, relative_std, seed)                 pipelines.hpp:119-132
+    l2_residual(a, b, grad=None) -> float                        graph.hpp:345-353, 498-509
+    tv_step(x, grad, out, lambda, lr) -> float                   graph.hpp:365-377, 511-546
+
+The reference's ``tv_reconstruct`` is typed for ParallelGeometry; its graph
+nodes take any geometry (graph.hpp:117-135), so here every geometry type
+(parallel, fan, cone) runs the same loop — the cone case is BASELINE config
+c5.  The whole loop is device resident (K2/K1 or K5-K7, then K8 residual and
+K9 fused TV + descent); only the loss history returns to the host.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import List, Tuple
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .containers import Image, Sinogram, is_host, require_f32, stream_of
+from .geometry import ConeGeometry, FanGeometry, ParallelGeometry, check
+from .projector import _check_cone_sino, _check_planar_sino, _dev
+
+
+@dataclass
+class ExperimentConfig:
+    """pipelines.hpp:156-164"""
+    phantom: str = "shepp-logan"
+    noise_relative_std: float = 0.0
+    learning_rate: float = 1e-3
+    iterations: int = 100
+    tv_lambda: float = 0.0
+    seed: int = 1337
+    filter_window: int = 0
+
+
+@dataclass
+class TvResult:
+    """pipelines.hpp:264-270"""
+    phantom: Image = None
+    noisy_sinogram: Sinogram = None
+    reconstruction: Image = None
+    fbp_reference: Image = None
+    loss_history: List[float] = field(default_factory=list)
+
+
+def add_gaussian_noise(sino: Sinogram, relative_std: float, seed: int) -> Sinogram:
+    """pipelines.hpp:119-132: additive white noise, sigma = relative_std *
+    max(sino), from the reference's mt19937_64 Box-Muller stream (bit-exact,
+    host)."""
+    data = sino.data
+    on_dev = isinstance(data, torch.Tensor)
+    host = np.ascontiguousarray(data.detach().cpu().numpy() if on_dev else data, dtype=np.float32)
+    out = np.empty_like(host)
+    N.check(N.lib().tg_add_gaussian_noise(host.ctypes.data, out.ctypes.data, host.size,
+                                          float(relative_std), int(seed)))
+    new = torch.from_numpy(out).to(data.device) if on_dev else out
+    s = Sinogram.__new__(Sinogram)
+    s.__dict__.update(sino.__dict__)
+    s.data = new
+    return s
+
+
+def l2_residual(a: torch.Tensor, b: torch.Tensor, grad: torch.Tensor = None) -> float:
+    """graph.hpp:345-353 value sum (a - b)^2 (FP64, deterministic); with
+    ``grad`` also writes the l2 gradient 2 (a - b) (graph.hpp:498-509)."""
+    check(a.shape == b.shape, "l2_loss expects matching shapes")
+    a, b = require_f32(a, "a"), require_f32(b, "b")
+    out = torch.empty(1, dtype=torch.float64, device=a.device)
+    N.check(N.lib().tg_l2_residual(a.data_ptr(), b.data_ptr(),
+                                   grad.data_ptr() if grad is not None else None, a.numel(),
+                                   out.data_ptr(), stream_of(a)))
+    return float(out.item())
+
+
+def tv_step(x: torch.Tensor, grad: torch.Tensor = None, out: torch.Tensor = None,
+            tv_lambda: float = 0.0, learning_rate: float = 0.0, has_lo: bool = False,
+            has_hi: bool = False, x_base: torch.Tensor = None) -> float:
+    """graph.hpp:365-377 TV value, 511-528 subgradient, 533-546 descent, fused:
+    out = x - lr (tv_lambda * dTV(x) + grad); returns TV(x) (FP64).  ``x`` is a
+    [ny][nx] image or a [nz][ny][nx] block; for a z-slab of a full replica pass
+    the slab view as ``x`` and has_lo / has_hi when the neighbouring slices
+    exist in the same storage."""
+    x = require_f32(x, "x")
+    check(x.is_contiguous(), "tv_step expects a contiguous block")
+    nz, ny, nx = (1,) + tuple(x.shape) if x.dim() == 2 else tuple(x.shape)
+    if has_lo or has_hi:
+        base = x_base if x_base is not None else x
+        lo = x.data_ptr() - base.data_ptr()
+        check(not has_lo or lo >= 4 * nx * ny, "tv_step: no slice before the block")
+        check(not has_hi or lo + 4 * x.numel() + 4 * nx * ny <= 4 * base.numel(),
+              "tv_step: no slice after the block")
+    v = torch.empty(1, dtype=torch.float64, device=x.device)
+    N.check(N.lib().tg_tv_step(x.data_ptr(), grad.data_ptr() if grad is not None else None,
+                               out.data_ptr() if out is not None else None, nx, ny, nz,
+                               int(has_lo), int(has_hi), float(tv_lambda), float(learning_rate),
+                               v.data_ptr(), stream_of(x)))
+    return float(v.item())
+
+
+def tv_reconstruct(sino: Sinogram, geo, cfg: ExperimentConfig,
+                   init: torch.Tensor = None) -> Tuple[Image, List[float]]:
+    """pipelines.hpp:273-299: min_x |Ax - p|^2 + tv_lambda TV(x), plain
+    gradient descent from zero (or ``init``), cfg.iterations steps at
+    cfg.learning_rate; returns the image and the iterations + 1 losses.
+    Raises the reference's "optimization diverged ..." Error on a non-finite
+    loss."""
+    data = require_f32(sino.data, "sinogram data")
+    on_host = is_host(data)
+    if on_host:
+        data = torch.from_numpy(np.ascontiguousarray(data)).cuda()
+    L = N.lib()
+    x = torch.zeros(geo.volume.torch_shape, dtype=torch.float32, device=data.device)
+    if init is not None:
+        x.copy_(init)
+    hist = np.zeros(int(cfg.iterations) + 1, np.float64)
+    args = (data.data_ptr(), x.data_ptr(), int(cfg.iterations), float(cfg.learning_rate),
+            float(cfg.tv_lambda), hist.ctypes.data_as(N.c_dblp), stream_of(data))
+    if isinstance(geo, ConeGeometry):
+        _check_cone_sino(sino, geo)
+        N.check(L.tg_cone_tv_reconstruct(geo._plan(_dev(data)), *args))
+    else:
+        check(isinstance(geo, (ParallelGeometry, FanGeometry)), "unknown geometry type")
+        _check_planar_sino(sino, geo)
+        N.check(L.tg_planar_tv_reconstruct(geo._plan(_dev(data)), *args))
+    img = Image(geo.volume, x.cpu().numpy() if on_host else x)
+    return img, hist.tolist()
+
+
+def make_phantom_2d(name: str, vol, device=None) -> Image:
+    """pipelines.hpp:166-172"""
+    from .phantom import disk_phantom, shepp_logan_2d
+    if name == "shepp-logan":
+        return shepp_logan_2d(vol, device)
+    if name == "disk":
+        # phantom.hpp:124-128 fov_half_extent
+        h = vol.extent(0)
+        for a in range(1, vol.dims()):
+            h = min(h, vol.extent(a))
+        return disk_phantom(vol, 0.4 * 2.0 * (0.5 * h), 1.0, device)
+    raise N.Error("unknown phantom: " + name)
+
+
+def experiment_iterative_tv(geo: ParallelGeometry, cfg: ExperimentConfig, device=None) -> TvResult:
+    """pipelines.hpp:301-312: phantom -> forward projection -> noise -> FBP
+    reference and TV reconstruction, all on the device."""
+    from .pipelines import FilterKind, fbp_reconstruct
+    from .projector import forward_project
+    r = TvResult()
+    r.phantom = make_phantom_2d(cfg.phantom, geo.volume, device)
+    sino = forward_project(r.phantom, geo)
+    r.noisy_sinogram = add_gaussian_noise(sino, cfg.noise_relative_std, cfg.seed)
+    r.fbp_reference = fbp_reconstruct(r.noisy_sinogram, geo, FilterKind.ramlak)
+    r.reconstruction, r.loss_history = tv_reconstruct(r.noisy_sinogram, geo, cfg)
+    return r
