@@ -206,6 +206,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--fp-steps", type=int, default=3)
+    ap.add_argument("--c5-iters", type=int, default=2,
+                    help="TV-loop iterations timed at config c5 (0 = skip the c5 leg)")
     args = ap.parse_args()
     assert args.warmup >= 3 or args.impl == "reference" or True
     if args.impl == "reference":
@@ -339,6 +341,8 @@ def main():
     e2e_s = max_over_ranks(time.perf_counter() - t0)
     e2e_value = updates_total * e2e_n / e2e_s / 1e9
     # the host call back-projects with scale 1; the timed K1 carried the FDK constant
+    e2e_h2d = int(h_band.numel() * 4) * world
+    e2e_d2h = int(h_slab.numel() * 4) * world
     e2e_parity = float((h_slab.to(dev) * scale - slab).abs().max() / slab.abs().max().clamp_min(1e-30))
 
     # ---- roofline (K1) --------------------------------------------------------
@@ -392,6 +396,14 @@ def main():
             cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
                    "sample": f"failed: {e}"}
 
+    # ---- config c5: iterative TV loop (1024^3, 720 x [2048 x 1536]) ----------
+    c5 = None
+    if args.c5_iters > 0:
+        del h_band, h_slab, band, raw_band, slab, part
+        torch.cuda.empty_cache()
+        c5 = run_c5(tg, D, torch, dist, dev, rank, world, backend, args.c5_iters, max_over_ranks,
+                    barrier)
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -401,8 +413,8 @@ def main():
             "config": {"workload": CONFIG_NAME, "parallelism": f"z-slab x{world}",
                        "slab_rows": [me.v0, me.n_rows], "l2": "inputs larger than L2 (2.38 GB sino, 512 MB volume)"},
             "e2e": {"value": e2e_value, "unit": UNIT,
-                    "h2d_bytes_per_step": int(h_band.numel() * 4) * world,
-                    "d2h_bytes_per_step": int(h_slab.numel() * 4) * world,
+                    "h2d_bytes_per_step": e2e_h2d,
+                    "d2h_bytes_per_step": e2e_d2h,
                     "path": "tg_cone_backproject_slab_host (pinned host band -> device, chunked "
                             "H2D overlapped with K1, D2H of the slab)", "max_rel_diff_vs_device": e2e_parity},
             "fp": {"metric": "cone forward projection Gsamples/s (c4, Shepp-Logan)",
@@ -413,10 +425,67 @@ def main():
             "k3_fdk_prefilter_ms": k3_ms, "k1_ms_mean": k1_avg, "k1_ms_min": min(k1_ms),
             "roofline": roofline, "clocks": clocks, "gpu_launches": gpu_launches,
             "cpu_baseline": cpu,
+            "c5_tv": c5,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+C5 = dict(n=1024, spacing=0.25, nu=2048, nv=1536, det=0.4, views=720, range_deg=360.0, sid=750.0,
+          sdd=1200.0, lr=2e-7, tv_lambda=0.05)
+C5_SAMPLES = 1.614458e12  # exact sum over rays of the reference's sample count
+
+
+def run_c5(tg, D, torch, dist, dev, rank, world, backend, iters, max_over_ranks, barrier):
+    """BASELINE config c5: the TV-regularised cone-beam loop (pipelines.hpp:
+    273-299 over a cone geometry) at 1024^3, 720 views of 2048 x 1536, on the
+    Shepp-Logan phantom.  N = 1: the device-resident C ABI loop
+    (tg_cone_tv_reconstruct); N > 1: the sharded loop (angle-sharded K2, band
+    all_to_all, slab K1, halo K9, slab all_gather over NCCL).  A call with I
+    iterations runs I (forward, backward, step) rounds plus one final forward
+    for the last loss, so seconds per iteration = (T(I) - T(0)) / I, both
+    device-timed with CUDA events (max over ranks)."""
+    vol = tg.VolumeSpec.centered([C5["n"]] * 3, [C5["spacing"]] * 3)
+    det = tg.Detector2D.centered(C5["nu"], C5["nv"], C5["det"], C5["det"])
+    geo = tg.make_cone(vol, det, C5["views"], C5["range_deg"] * math.pi / 180.0, C5["sid"],
+                       C5["sdd"])
+    views = D.view_partition(geo, world)
+    vw0, vwn = views[rank]
+    ph = tg.shepp_logan_3d(vol, device=dev).data
+    p = tg.cone_forward_views(geo, ph, vw0, vwn)
+    del ph
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream(dev)
+    cfg_name = ("c5: iterative TV cone loop, 1024^3 @0.25mm, 720 x [2048 x 1536] @0.4mm, 360 deg, "
+                f"SID 750 / SDD 1200, lr {C5['lr']}, tv_lambda {C5['tv_lambda']}")
+
+    def timed(n_it):
+        barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        if world == 1:
+            cfg = tg.ExperimentConfig(learning_rate=C5["lr"], iterations=n_it,
+                                      tv_lambda=C5["tv_lambda"])
+            sino = tg.Sinogram.cone_beam(geo.n_projections, det, data=p)
+            _, hist = tg.tv_reconstruct(sino, geo, cfg)
+        else:
+            _, hist = D.tv_reconstruct_sharded(geo, p, n_it, C5["lr"], C5["tv_lambda"])
+        b.record(stream)
+        torch.cuda.synchronize()
+        return max_over_ranks(a.elapsed_time(b)), hist
+
+    timed(0)  # warm: plan buffers, the allocator pool, constant banks
+    t0, _ = timed(0)
+    tI, hist = timed(iters)
+    s_per_it = (tI - t0) / iters / 1e3
+    updates = float(C5["n"]) ** 3 * C5["views"]
+    return {"workload": cfg_name, "iterations": iters, "s_per_iter": s_per_it,
+            "final_forward_s": t0 / 1e3,
+            "fp_plus_bp_units_per_s": {"Gsamples": C5_SAMPLES / s_per_it / 1e9,
+                                       "GUPS": updates / s_per_it / 1e9},
+            "loss_history": hist, "path": "tg_cone_tv_reconstruct" if world == 1 else
+            "distributed.tv_reconstruct_sharded (NCCL all_to_all + all_gather)"}
 
 
 _SAMPLES_CACHE = os.path.join(ROOT, "profiles", "c4_samples.json")
