@@ -441,8 +441,10 @@ def run_c5(tg, D, torch, dist, dev, rank, world, backend, iters, max_over_ranks,
     """BASELINE config c5: the TV-regularised cone-beam loop (pipelines.hpp:
     273-299 over a cone geometry) at 1024^3, 720 views of 2048 x 1536, on the
     Shepp-Logan phantom.  N = 1: the device-resident C ABI loop
-    (tg_cone_tv_reconstruct); N > 1: the sharded loop (angle-sharded K2, band
-    all_to_all, slab K1, halo K9, slab all_gather over NCCL).  A call with I
+    (tg_cone_tv_reconstruct); N > 1 on one node: the fused loop (angle-sharded
+    K2, K8 storing residual row bands into the slab owners' buffers, slab K1,
+    K9 storing the updated slab into every replica — peer stores over NVLink);
+    across nodes the NCCL loop (all_to_all + all_gather).  A call with I
     iterations runs I (forward, backward, step) rounds plus one final forward
     for the last loss, so seconds per iteration = (T(I) - T(0)) / I, both
     device-timed with CUDA events (max over ranks)."""
@@ -452,6 +454,9 @@ def run_c5(tg, D, torch, dist, dev, rank, world, backend, iters, max_over_ranks,
                        C5["sdd"])
     views = D.view_partition(geo, world)
     vw0, vwn = views[rank]
+    # all ranks on one node (NVSwitch): exchanges fused into the kernels as
+    # CUDA-IPC peer stores; across nodes: NCCL all_to_all / all_gather
+    single_node = int(os.environ.get("LOCAL_WORLD_SIZE", world)) == world
     ph = tg.shepp_logan_3d(vol, device=dev).data
     p = tg.cone_forward_views(geo, ph, vw0, vwn)
     del ph
@@ -469,6 +474,8 @@ def run_c5(tg, D, torch, dist, dev, rank, world, backend, iters, max_over_ranks,
                                       tv_lambda=C5["tv_lambda"])
             sino = tg.Sinogram.cone_beam(geo.n_projections, det, data=p)
             _, hist = tg.tv_reconstruct(sino, geo, cfg)
+        elif single_node:
+            _, hist = D.tv_reconstruct_p2p(geo, p, n_it, C5["lr"], C5["tv_lambda"])
         else:
             _, hist = D.tv_reconstruct_sharded(geo, p, n_it, C5["lr"], C5["tv_lambda"])
         b.record(stream)
@@ -485,7 +492,9 @@ def run_c5(tg, D, torch, dist, dev, rank, world, backend, iters, max_over_ranks,
             "fp_plus_bp_units_per_s": {"Gsamples": C5_SAMPLES / s_per_it / 1e9,
                                        "GUPS": updates / s_per_it / 1e9},
             "loss_history": hist, "path": "tg_cone_tv_reconstruct" if world == 1 else
-            "distributed.tv_reconstruct_sharded (NCCL all_to_all + all_gather)"}
+            ("distributed.tv_reconstruct_p2p (K8 residual scatter + K9 slab broadcast as "
+             "CUDA-IPC peer stores)" if single_node else
+             "distributed.tv_reconstruct_sharded (NCCL all_to_all + all_gather)")}
 
 
 _SAMPLES_CACHE = os.path.join(ROOT, "profiles", "c4_samples.json")

@@ -250,6 +250,31 @@ tg_status tg_l2_residual(const float* d_a, const float* d_b, float* d_grad, uint
 tg_status tg_tv_step(const float* d_x, const float* d_grad, float* d_x_out, uint64_t nx,
                      uint64_t ny, uint64_t nz, int has_lo, int has_hi, double tv_lambda,
                      double learning_rate, double* d_tv, void* stream);
+/* Multi-GPU forms of the same kernels with the exchange fused in (SURVEY §8e,
+ * config c5): destinations may be peer buffers mapped through CUDA IPC, so the
+ * stores travel over NVLink / NVSwitch as the values are computed.
+ * tg_l2_residual_scatter: K8 over this rank's views [view0, view0 + n_views) of
+ * [n_v][n_u] projections, each residual row stored into every band that holds
+ * it (band d: [n_proj][n_rows_d][n_u], rows [v0_d, v0_d + n_rows_d)).
+ * tg_tv_step_multi: K9 with the updated block stored to 1..16 destinations. */
+typedef struct tg_band_dest {
+  float* band;
+  uint64_t v0, n_rows;
+} tg_band_dest;
+tg_status tg_l2_residual_scatter(const float* d_fp, const float* d_p, uint64_t n_views,
+                                 uint64_t n_v, uint64_t n_u, uint64_t view0,
+                                 const tg_band_dest* dests, int n_dests, double* d_sum,
+                                 void* stream);
+tg_status tg_tv_step_multi(const float* d_x, const float* d_grad, float* const* d_x_outs, int n_out,
+                           uint64_t nx, uint64_t ny, uint64_t nz, int has_lo, int has_hi,
+                           double tv_lambda, double learning_rate, double* d_tv, void* stream);
+/* device buffers shareable with the other ranks of a node (cudaMalloc bases,
+ * zero-filled), their 64-byte CUDA IPC handles, and peer mappings */
+tg_status tg_device_alloc(uint64_t bytes, int device, void** d_ptr);
+tg_status tg_device_free(void* d_ptr);
+tg_status tg_ipc_get_handle(const void* d_base, unsigned char* out64);
+tg_status tg_ipc_open_handle(const unsigned char* in64, int device, void** d_ptr);
+tg_status tg_ipc_close_handle(void* d_ptr);
 /* pipelines.hpp:273-299 tv_reconstruct (graph: x -> forward_project -> l2_loss(., p)
  * + tv_lambda * tv_loss(x), plain gradient descent), on any geometry, device
  * resident: d_x holds the initial image (the reference starts from zero) and

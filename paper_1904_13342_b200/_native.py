@@ -47,6 +47,10 @@ class tg_cone_geometry(C.Structure):
                 ("sources", c_dblp), ("inv_blocks", c_dblp), ("angles", c_dblp)]
 
 
+class tg_band_dest(C.Structure):
+    _fields_ = [("band", c_vp), ("v0", c_u64), ("n_rows", c_u64)]
+
+
 _P = C.POINTER
 # name -> (restype, argtypes); mirrors include/tomograd_b200.h one to one
 SIGNATURES = {
@@ -105,6 +109,15 @@ SIGNATURES = {
     "tg_l2_residual": (c_int, [c_vp, c_vp, c_vp, c_u64, c_vp, c_vp]),
     "tg_tv_step": (c_int, [c_vp, c_vp, c_vp, c_u64, c_u64, c_u64, c_int, c_int, c_dbl, c_dbl, c_vp,
                            c_vp]),
+    "tg_l2_residual_scatter": (c_int, [c_vp, c_vp, c_u64, c_u64, c_u64, c_u64, _P(tg_band_dest),
+                                       c_int, c_vp, c_vp]),
+    "tg_tv_step_multi": (c_int, [c_vp, c_vp, _P(c_vp), c_int, c_u64, c_u64, c_u64, c_int, c_int,
+                                 c_dbl, c_dbl, c_vp, c_vp]),
+    "tg_device_alloc": (c_int, [c_u64, c_int, _P(c_vp)]),
+    "tg_device_free": (c_int, [c_vp]),
+    "tg_ipc_get_handle": (c_int, [c_vp, _P(C.c_ubyte)]),
+    "tg_ipc_open_handle": (c_int, [_P(C.c_ubyte), c_int, _P(c_vp)]),
+    "tg_ipc_close_handle": (c_int, [c_vp]),
     "tg_cone_tv_reconstruct": (c_int, [c_vp, c_vp, c_vp, c_u64, c_dbl, c_dbl, c_dblp, c_vp]),
     "tg_planar_tv_reconstruct": (c_int, [c_vp, c_vp, c_vp, c_u64, c_dbl, c_dbl, c_dblp, c_vp]),
     "tg_add_gaussian_noise": (c_int, [c_vp, c_vp, c_u64, c_dbl, c_u64]),

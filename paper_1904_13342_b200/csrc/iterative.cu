@@ -20,6 +20,7 @@
 //    update fused; x is double-buffered.  HBM-bound: 12 B per voxel
 //    (x, grad in; x' out), neighbour re-reads hit L1/L2.
 #include <cmath>
+#include <cstring>
 #include <string>
 #include <vector>
 
@@ -86,8 +87,16 @@ __device__ __forceinline__ int sgn(double d) { return (d > 0.0) - (d < 0.0); }
 // and the TV of the forward pairs (i, i + s_a) it owns.  Differences of fp32
 // values are exact in FP64, so signs and |d| are exactly the reference's for
 // the same x.  x_out == nullptr: value only.
+// Destinations of one computed value: the local buffer and / or peer buffers
+// mapped through CUDA IPC (NVLink / NVSwitch stores on a multi-GPU node).
+constexpr int kMaxDest = 16;
+struct OutList {
+  float* p[kMaxDest];
+  int n;
+};
+
 __global__ void __launch_bounds__(kRedThreads) tv_step_kernel(
-    const float* __restrict__ x, const float* __restrict__ grad, float* __restrict__ x_out, int nx,
+    const float* __restrict__ x, const float* __restrict__ grad, const OutList outs, int nx,
     int ny, int nz, int has_lo, int has_hi, double lambda, double lr, double* __restrict__ partial) {
   const long long plane = (long long)nx * ny;
   const long long n = plane * nz;
@@ -117,9 +126,11 @@ __global__ void __launch_bounds__(kRedThreads) tv_step_kernel(
       s -= sgn(d);
       tv += fabs(d);
     }
-    if (x_out) {
+    if (outs.n) {
       const double g = lambda * double(s) + double(grad[i]);
-      x_out[i] = float(xi - lr * g);
+      const float v = float(xi - lr * g);
+#pragma unroll 1
+      for (int d = 0; d < outs.n; ++d) outs.p[d][i] = v;  // local and / or peer replicas
     }
   }
   tv = block_sum(tv);
@@ -143,6 +154,48 @@ struct Scratch {
   explicit Scratch(cudaStream_t s) : buf(kRedBlocks, s), partial(buf.p) {}
 };
 
+OutList one_out(float* p) {
+  OutList o;
+  o.n = p ? 1 : 0;
+  o.p[0] = p;
+  return o;
+}
+
+// K8 with the exchange fused in: g = 2 (fp - p) of this rank's views, each
+// row stored straight into the row band of every slab owner that needs it
+// (peer buffers through IPC: the all_to_all of the sharded loop without a
+// separate collective or staging copy).  fp is [n_views][nv][nu]; band d
+// is [n_proj][n_rows_d][nu] holding rows [v0_d, v0_d + n_rows_d).
+struct BandList {
+  float* p[kMaxDest];
+  int v0[kMaxDest], n_rows[kMaxDest];
+  int n;
+};
+
+__global__ void __launch_bounds__(kRedThreads) l2_scatter_kernel(
+    const float* __restrict__ fp, const float* __restrict__ pm, uint64_t n, int nv, int nu,
+    int view0, const BandList bands, double* __restrict__ partial) {
+  double acc = 0.0;
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const double d = double(fp[i]) - double(pm[i]);
+    acc += d * d;
+    const float g = float(2.0 * d);
+    const int u = int(i % nu);
+    const uint64_t rv = i / nu;
+    const int r = int(rv % nv);
+    const long long view = (long long)(rv / nv) + view0;
+#pragma unroll 1
+    for (int b = 0; b < bands.n; ++b) {
+      const int rr = r - bands.v0[b];
+      if (rr >= 0 && rr < bands.n_rows[b])
+        bands.p[b][(view * bands.n_rows[b] + rr) * nu + u] = g;
+    }
+  }
+  acc = block_sum(acc);
+  if (threadIdx.x == 0) partial[blockIdx.x] = acc;
+}
+
 void l2_residual(const float* a, const float* b, float* g, uint64_t n, double* d_sum,
                  cudaStream_t st, const Scratch& sc) {
   l2_residual_kernel<<<kRedBlocks, kRedThreads, 0, st>>>(a, b, g, n, 2.0 * 1.0, sc.partial);
@@ -150,10 +203,10 @@ void l2_residual(const float* a, const float* b, float* g, uint64_t n, double* d
   TG_LAUNCHED(2);
 }
 
-void tv_step(const float* x, const float* grad, float* x_out, uint64_t nx, uint64_t ny, uint64_t nz,
-             int has_lo, int has_hi, double lambda, double lr, double* d_tv, cudaStream_t st,
-             const Scratch& sc) {
-  tv_step_kernel<<<kRedBlocks, kRedThreads, 0, st>>>(x, grad, x_out, int(nx), int(ny), int(nz),
+void tv_step(const float* x, const float* grad, const OutList& outs, uint64_t nx, uint64_t ny,
+             uint64_t nz, int has_lo, int has_hi, double lambda, double lr, double* d_tv,
+             cudaStream_t st, const Scratch& sc) {
+  tv_step_kernel<<<kRedBlocks, kRedThreads, 0, st>>>(x, grad, outs, int(nx), int(ny), int(nz),
                                                       has_lo, has_hi, lambda, lr, sc.partial);
   sum_partials_kernel<<<1, kRedThreads, 0, st>>>(sc.partial, kRedBlocks, d_tv);
   TG_LAUNCHED(2);
@@ -178,12 +231,13 @@ void tv_loop(Fwd fwd, Bwd bwd, uint64_t n_sino, uint64_t nx, uint64_t ny, uint64
     fwd(cur, fp);
     l2_residual(fp, d_sino, fp, n_sino, sums + 2 * it, st, sc);
     bwd(fp, bp);
-    tv_step(cur, bp, nxt, nx, ny, nz, 0, 0, lambda, lr, sums + 2 * it + 1, st, sc);
+    tv_step(cur, bp, one_out(nxt), nx, ny, nz, 0, 0, lambda, lr, sums + 2 * it + 1, st, sc);
     std::swap(cur, nxt);
   }
   fwd(cur, fp);
   l2_residual(fp, d_sino, nullptr, n_sino, sums + 2 * iterations, st, sc);
-  tv_step(cur, nullptr, nullptr, nx, ny, nz, 0, 0, lambda, lr, sums + 2 * iterations + 1, st, sc);
+  tv_step(cur, nullptr, one_out(nullptr), nx, ny, nz, 0, 0, lambda, lr, sums + 2 * iterations + 1,
+          st, sc);
   if (cur != d_x)
     TG_CUDA(cudaMemcpyAsync(d_x, cur, n_vox * sizeof(float), cudaMemcpyDeviceToDevice, st));
   std::vector<double> s(2 * (iterations + 1));
@@ -225,9 +279,91 @@ tg_status tg_tv_step(const float* d_x, const float* d_grad, float* d_x_out, uint
     check(d_x_out == nullptr || d_x_out != d_x, "tv_step: x_out must not alias x");
     const cudaStream_t st = as_stream(stream);
     iter::Scratch sc(st);
-    iter::tv_step(d_x, d_grad, d_x_out, nx, ny, nz, has_lo != 0, has_hi != 0, tv_lambda,
-                  learning_rate, d_tv, st, sc);
+    iter::tv_step(d_x, d_grad, iter::one_out(d_x_out), nx, ny, nz, has_lo != 0, has_hi != 0,
+                  tv_lambda, learning_rate, d_tv, st, sc);
   });
+}
+
+tg_status tg_tv_step_multi(const float* d_x, const float* d_grad, float* const* d_x_outs, int n_out,
+                           uint64_t nx, uint64_t ny, uint64_t nz, int has_lo, int has_hi,
+                           double tv_lambda, double learning_rate, double* d_tv, void* stream) {
+  return guarded([&] {
+    check(nx >= 1 && ny >= 1 && nz >= 1, "tv_loss needs a non-scalar input");
+    check(n_out >= 1 && n_out <= iter::kMaxDest && d_grad != nullptr,
+          "tv_step_multi: 1..16 destinations and a gradient");
+    iter::OutList o;
+    o.n = n_out;
+    for (int d = 0; d < n_out; ++d) {
+      check(d_x_outs[d] != nullptr && d_x_outs[d] != d_x, "tv_step: x_out must not alias x");
+      o.p[d] = d_x_outs[d];
+    }
+    const cudaStream_t st = as_stream(stream);
+    iter::Scratch sc(st);
+    iter::tv_step(d_x, d_grad, o, nx, ny, nz, has_lo != 0, has_hi != 0, tv_lambda, learning_rate,
+                  d_tv, st, sc);
+  });
+}
+
+tg_status tg_l2_residual_scatter(const float* d_fp, const float* d_p, uint64_t n_views,
+                                 uint64_t n_v, uint64_t n_u, uint64_t view0,
+                                 const tg_band_dest* dests, int n_dests, double* d_sum,
+                                 void* stream) {
+  return guarded([&] {
+    check(n_views >= 1 && n_v >= 1 && n_u >= 1, "l2_loss expects matching shapes");
+    check(n_dests >= 1 && n_dests <= iter::kMaxDest, "residual scatter: 1..16 destinations");
+    iter::BandList b;
+    b.n = n_dests;
+    for (int d = 0; d < n_dests; ++d) {
+      check(dests[d].band != nullptr && dests[d].v0 + dests[d].n_rows <= n_v,
+            "detector row band lies outside the detector");
+      b.p[d] = dests[d].band;
+      b.v0[d] = int(dests[d].v0);
+      b.n_rows[d] = int(dests[d].n_rows);
+    }
+    const cudaStream_t st = as_stream(stream);
+    iter::Scratch sc(st);
+    iter::l2_scatter_kernel<<<iter::kRedBlocks, iter::kRedThreads, 0, st>>>(
+        d_fp, d_p, n_views * n_v * n_u, int(n_v), int(n_u), int(view0), b, sc.partial);
+    iter::sum_partials_kernel<<<1, iter::kRedThreads, 0, st>>>(sc.partial, iter::kRedBlocks, d_sum);
+    TG_LAUNCHED(2);
+  });
+}
+
+// ---- peer memory (CUDA IPC) for the fused multi-GPU exchanges -------------
+
+tg_status tg_device_alloc(uint64_t bytes, int device, void** d_ptr) {
+  return guarded([&] {
+    DeviceGuard dg(device);
+    *d_ptr = nullptr;
+    TG_CUDA(cudaMalloc(d_ptr, bytes));
+    TG_CUDA(cudaMemset(*d_ptr, 0, bytes));
+  });
+}
+
+tg_status tg_device_free(void* d_ptr) {
+  return guarded([&] { TG_CUDA(cudaFree(d_ptr)); });
+}
+
+tg_status tg_ipc_get_handle(const void* d_base, unsigned char* out64) {
+  return guarded([&] {
+    cudaIpcMemHandle_t h;
+    TG_CUDA(cudaIpcGetMemHandle(&h, const_cast<void*>(d_base)));
+    static_assert(sizeof(h) == 64, "IPC handle size");
+    std::memcpy(out64, &h, 64);
+  });
+}
+
+tg_status tg_ipc_open_handle(const unsigned char* in64, int device, void** d_ptr) {
+  return guarded([&] {
+    DeviceGuard dg(device);
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, in64, 64);
+    TG_CUDA(cudaIpcOpenMemHandle(d_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  });
+}
+
+tg_status tg_ipc_close_handle(void* d_ptr) {
+  return guarded([&] { TG_CUDA(cudaIpcCloseMemHandle(d_ptr)); });
 }
 
 tg_status tg_cone_tv_reconstruct(tg_cone_plan* plan, const float* d_sino, float* d_x,

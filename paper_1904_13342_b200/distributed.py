@@ -244,3 +244,157 @@ def tv_reconstruct_sharded(geo: ConeGeometry, p_part: torch.Tensor, iterations: 
         if not last:
             gather_slabs_into(xs, shards, x, group)
     return x, hist
+
+
+# ---------------------------------------------------------------------------
+# single-node fused path: the exchanges as peer stores inside the kernels
+
+
+def _device_view(ptr: int, shape, device) -> torch.Tensor:
+    """zero-copy float32 tensor over a raw device pointer"""
+    class _A:
+        __cuda_array_interface__ = {"shape": tuple(int(v) for v in shape), "typestr": "<f4",
+                                    "data": (int(ptr), False), "version": 3, "strides": None}
+    return torch.as_tensor(_A(), device=device)
+
+
+class PeerBuffers:
+    """Device buffers of this rank that every rank of the node maps through
+    CUDA IPC (tg_device_alloc + tg_ipc_*), with the peers' mappings."""
+
+    def __init__(self, nbytes: List[int], device: int, group=None):
+        L = N.lib()
+        self.device = device
+        self.own = []
+        for nb in nbytes:
+            p = C.c_void_p()
+            N.check(L.tg_device_alloc(int(nb), device, C.byref(p)))
+            self.own.append(p.value)
+        handles = []
+        for p in self.own:
+            h = (C.c_ubyte * 64)()
+            N.check(L.tg_ipc_get_handle(p, h))
+            handles.append(bytes(h))
+        world = dist.get_world_size(group)
+        everyone = [None] * world
+        dist.all_gather_object(everyone, handles, group=group)
+        me = dist.get_rank(group)
+        self.peer = []  # peer[r][i]: buffer i of rank r in this process
+        self._opened = []
+        for r in range(world):
+            if r == me:
+                self.peer.append(list(self.own))
+                continue
+            ptrs = []
+            for hb in everyone[r]:
+                p = C.c_void_p()
+                h = (C.c_ubyte * 64).from_buffer_copy(hb)
+                N.check(L.tg_ipc_open_handle(h, device, C.byref(p)))
+                ptrs.append(p.value)
+                self._opened.append(p.value)
+            self.peer.append(ptrs)
+
+    def close(self):
+        L = N.lib()
+        for p in self._opened:
+            L.tg_ipc_close_handle(p)
+        self._opened = []
+        for p in self.own:
+            L.tg_device_free(p)
+        self.own = []
+
+
+def tv_reconstruct_p2p(geo: ConeGeometry, p_part: torch.Tensor, iterations: int,
+                       learning_rate: float, tv_lambda: float, group=None,
+                       align: int = Z_ALIGN):
+    """The config-5 loop on one node with both exchanges fused into the
+    kernels that produce the data (no NCCL data-path collective):
+
+    * K8 scatter (tg_l2_residual_scatter) stores every residual row of this
+      rank's views straight into the row band of each slab owner that needs it
+      (peer memory over NVLink / NVSwitch);
+    * K9 broadcast (tg_tv_step_multi) stores the updated slab into the next
+      volume replica of every rank.
+    Replicas are double-buffered (ranks read x_i while peers write x_{i+1});
+    a stream sync + barrier separates the phases.  Bitwise equal to
+    tv_reconstruct_sharded and to the single-GPU loop."""
+    from ._native import Error
+    L = N.lib()
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    dev = p_part.device
+    dix = dev.index if dev.index is not None else torch.cuda.current_device()
+    shards = slab_shards(geo, world, align)
+    views = view_partition(geo, world)
+    me = shards[rank]
+    vw0, vwn = views[rank]
+    nx, ny, nz = geo.volume.shape
+    nu, nv = geo.detector.n_u, geo.detector.n_v
+    plane = nx * ny
+    vol_bytes = 4 * nx * ny * nz
+    band_bytes = 4 * geo.n_projections * me.n_rows * nu
+    bufs = PeerBuffers([band_bytes, vol_bytes, vol_bytes], dix, group)
+    plan = geo._plan(dix)
+    st = torch.cuda.current_stream(dev).cuda_stream
+    fp = torch.empty((vwn, nv, nu), dtype=torch.float32, device=dev)
+    bp = torch.empty((me.nz, ny, nx), dtype=torch.float32, device=dev)
+    sums = torch.zeros(2 * (iterations + 1), dtype=torch.float64, device=dev)
+    p_part = p_part.contiguous()
+    dests = (N.tg_band_dest * world)(*[N.tg_band_dest(bufs.peer[r][0], s.v0, s.n_rows)
+                                       for r, s in enumerate(shards)])
+    band = bufs.own[0]
+    cur, nxt = 1, 2
+
+    def sync_all():
+        torch.cuda.current_stream(dev).synchronize()
+        dist.barrier(group=group)
+
+    try:
+        sync_all()  # every rank's buffers exist and are zero
+        for it in range(iterations + 1):
+            last = it == iterations
+            x_own = bufs.peer[rank][cur]
+            N.check(L.tg_cone_forward_views(plan, vw0, vwn, x_own, fp.data_ptr(), st))
+            d_sum = sums.data_ptr() + 8 * (2 * it)
+            d_tv = sums.data_ptr() + 8 * (2 * it + 1)
+            if last:
+                N.check(L.tg_l2_residual(fp.data_ptr(), p_part.data_ptr(), None, fp.numel(), d_sum, st))
+                N.check(L.tg_tv_step(x_own + 4 * me.z0 * plane, None, None, nx, ny, me.nz,
+                                     int(me.z0 > 0), int(me.z0 + me.nz < nz), float(tv_lambda),
+                                     float(learning_rate), d_tv, st))
+                break
+            N.check(L.tg_l2_residual_scatter(fp.data_ptr(), p_part.data_ptr(), vwn, nv, nu, vw0,
+                                             dests, world, d_sum, st))
+            sync_all()  # every band complete
+            N.check(L.tg_cone_backproject_slab(plan, me.z0, me.nz, me.v0, me.n_rows, band,
+                                               bp.data_ptr(), 1.0, 0, st))
+            outs = (C.c_void_p * world)(*[bufs.peer[r][nxt] + 4 * me.z0 * plane
+                                          for r in range(world)])
+            N.check(L.tg_tv_step_multi(x_own + 4 * me.z0 * plane, bp.data_ptr(), outs, world, nx,
+                                       ny, me.nz, int(me.z0 > 0), int(me.z0 + me.nz < nz),
+                                       float(tv_lambda), float(learning_rate), d_tv, st))
+            sync_all()  # every slab in every next replica
+            cur, nxt = nxt, cur
+        # loss partials of all ranks, summed in rank order
+        world_sums = [torch.empty_like(sums) for _ in range(world)]
+        if dist.get_backend(group) == "gloo":
+            host = sums.cpu()
+            tmp = [torch.empty_like(host) for _ in range(world)]
+            dist.all_gather(tmp, host, group=group)
+            world_sums = tmp
+        else:
+            dist.all_gather(world_sums, sums, group=group)
+        tot = torch.zeros(2 * (iterations + 1), dtype=torch.float64)
+        for w in world_sums:
+            tot += w.cpu()
+        hist = []
+        for it in range(iterations + 1):
+            loss = float(tot[2 * it]) + float(tot[2 * it + 1]) * tv_lambda
+            hist.append(loss)
+            if not math.isfinite(loss):
+                raise Error(f"optimization diverged at iteration {it} (loss is not finite); "
+                            "lower the learning rate")
+        x = _device_view(bufs.peer[rank][cur], (nz, ny, nx), dev).clone()
+        return x, hist
+    finally:
+        sync_all()
+        bufs.close()

@@ -224,3 +224,81 @@ def test_sharded_tv_world2_bitwise_equal_world1(tg):
     for rank, x, h in got:
         assert np.array_equal(x, want), f"rank {rank}"
         assert np.max(np.abs(np.array(h) - np.array(hist)) / np.array(hist)) <= 1e-12
+
+
+def _p2p_worker(rank, world, port, q):
+    import os
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    import torch.distributed as dist
+    import paper_1904_13342_b200 as tg
+    from paper_1904_13342_b200 import distributed as D
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)  # ranks share one GPU
+    try:
+        geo, sino = _c5_small(tg)
+        v0, vn = D.view_partition(geo, world)[rank]
+        x, hist = D.tv_reconstruct_p2p(geo, sino.data[v0:v0 + vn].contiguous(), 6, 2e-5, 0.3)
+        q.put((rank, x.cpu().numpy(), hist))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_p2p_fused_tv_world2_bitwise_equal_world1(tg):
+    """The fused-exchange loop (K8 scatter + K9 broadcast into CUDA-IPC peer
+    buffers): two processes on one GPU map each other's buffers through IPC
+    exactly as ranks on an NVSwitch node do."""
+    import socket
+    import torch.multiprocessing as mp
+    geo, sino = _c5_small(tg)
+    cfg = tg.ExperimentConfig(learning_rate=2e-5, iterations=6, tv_lambda=0.3)
+    img, hist = tg.tv_reconstruct(sino, geo, cfg)
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_p2p_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = [q.get(timeout=300) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    want = img.data.cpu().numpy()
+    for rank, x, h in got:
+        assert np.array_equal(x, want), f"rank {rank}"
+        assert np.max(np.abs(np.array(h) - np.array(hist)) / np.array(hist)) <= 1e-12
+
+
+def test_residual_scatter_and_multi_step_single_process(tg):
+    """K8 scatter into two row bands of local buffers, K9 into two outputs"""
+    fp = torch.from_numpy(rand((5, 12, 9), 11)).to(DEV)
+    p = torch.from_numpy(rand((5, 12, 9), 12)).to(DEV)
+    import ctypes as C
+    from paper_1904_13342_b200 import _native as N
+    bands = [torch.full((8, 6, 9), -7.0, device=DEV), torch.full((8, 5, 9), -7.0, device=DEV)]
+    dests = (N.tg_band_dest * 2)(N.tg_band_dest(bands[0].data_ptr(), 0, 6),
+                                 N.tg_band_dest(bands[1].data_ptr(), 7, 5))
+    s = torch.zeros(1, dtype=torch.float64, device=DEV)
+    st = torch.cuda.current_stream().cuda_stream
+    N.check(N.lib().tg_l2_residual_scatter(fp.data_ptr(), p.data_ptr(), 5, 12, 9, 2, dests, 2,
+                                           s.data_ptr(), st))
+    g = torch.empty_like(fp)
+    v = tg.l2_residual(fp, p, g)
+    assert float(s) == v
+    assert torch.equal(bands[0][2:7], g[:, 0:6]) and torch.equal(bands[1][2:7], g[:, 7:12])
+    assert bool((bands[0][:2] == -7).all()) and bool((bands[1][7:] == -7).all())
+    x = torch.from_numpy(rand((6, 7, 8), 13)).to(DEV)
+    gr = torch.from_numpy(rand((6, 7, 8), 14)).to(DEV)
+    one = torch.empty_like(x)
+    tv1 = tg.tv_step(x, gr, one, 0.5, 1e-2)
+    outs = [torch.empty_like(x), torch.empty_like(x)]
+    arr = (C.c_void_p * 2)(outs[0].data_ptr(), outs[1].data_ptr())
+    N.check(N.lib().tg_tv_step_multi(x.data_ptr(), gr.data_ptr(), arr, 2, 8, 7, 6, 0, 0, 0.5, 1e-2,
+                                     s.data_ptr(), st))
+    assert float(s) == tv1 and torch.equal(outs[0], one) and torch.equal(outs[1], one)
