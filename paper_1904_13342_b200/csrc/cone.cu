@@ -428,6 +428,11 @@ struct FpArgs {
   // (V[z][y][x], V[z][y][x+1], V[z][y+1][x], V[z][y+1][x+1]), so one
   // trilinear sample is two 16-byte gathers (slices z and z+1)
   const float4* __restrict__ vq;
+  // the same quads in y-fastest order (index y + x * nyp + z * nxp * nyp):
+  // views whose rays run mostly along x gather from it, so the 8 u-lanes of
+  // a warp (which then step along y) read neighbouring quads
+  const float4* __restrict__ vqT;
+  int dual;                       // use vqT for x-dominant rays
   int nxp, nyp;                   // padded extents (x, y)
   float* out;                     // [n_views][nv][nu]
 };
@@ -474,10 +479,12 @@ __device__ __forceinline__ float lerpf(float a, float b, float w) { return fmaf(
 // of streaming the whole volume from HBM once per view.
 // Each warp covers 8 u x 4 v pixels (its rays stay close together in 3D:
 // fewer cache lines per gather than a 32-wide row of pixels).
-__global__ void __launch_bounds__(256) cone_fp_kernel(const FpArgs a) {
+template <int TU>
+__global__ void __launch_bounds__(256, 4) cone_fp_kernel(const FpArgs a) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int iu = blockIdx.x * 32 + (w & 3) * 8 + (lane & 7);
-  const int iv = blockIdx.z * 8 + (w >> 2) * 4 + (lane >> 3);
+  constexpr int WPR = TU / 8;  // 8 u x 4 v warps, TU / 8 of them per 4-row band
+  const int iu = blockIdx.x * TU + (w % WPR) * 8 + (lane & 7);
+  const int iv = blockIdx.z * (256 / TU) + (w / WPR) * 4 + (lane >> 3);
   const int vl = blockIdx.y;
   if (iu >= a.nu || iv >= a.nv) return;
   const double* g = a.geo + 12 * (a.view0 + vl);
@@ -512,7 +519,10 @@ __global__ void __launch_bounds__(256) cone_fp_kernel(const FpArgs a) {
   const double p0z = (o[2] + th * d[2] - a.oz) / a.sz + 2.0;
   const double ddx = dt * d[0] / a.sx, ddy = dt * d[1] / a.sy, ddz = dt * d[2] / a.sz;
   const float fdx = float(ddx), fdy = float(ddy), fdz = float(ddz);
-  const int nxp = a.nxp, nxyp = a.nxp * a.nyp;
+  const int nxyp = a.nxp * a.nyp;
+  const bool xdom = a.dual && fabs(d[0]) > fabs(d[1]);
+  const float4* vbase = xdom ? a.vqT : a.vq;
+  const int sx = xdom ? a.nyp : 1, sy = xdom ? 1 : a.nxp;
   constexpr float MAGIC = 12582912.0f;  // 1.5 * 2^23: t = M + floor(p) under round-down
   constexpr int MAGIC_BITS = 0x4B400000;
   double total = 0.0;
@@ -524,7 +534,7 @@ __global__ void __launch_bounds__(256) cone_fp_kernel(const FpArgs a) {
                  az = p0z + double(k0) * ddz;
     const double cx = floor(ax), cy = floor(ay), cz = floor(az);
     const float bx = float(ax - cx), by = float(ay - cy), bz = float(az - cz);
-    const float4* cell = a.vq + (long long)cz * nxyp + (long long)cy * nxp + (long long)cx;
+    const float4* cell = vbase + (long long)cz * nxyp + (long long)cy * sy + (long long)cx * sx;
     const int m = int(min(64LL, n - k0));
     float sum = 0.0f;
     // samples advance by at most half a voxel, so consecutive samples often
@@ -540,7 +550,7 @@ __global__ void __launch_bounds__(256) cone_fp_kernel(const FpArgs a) {
       const float pz = fmaf(float(j), fdz, bz);
       const float tx = __fadd_rd(px, MAGIC), ty = __fadd_rd(py, MAGIC), tz = __fadd_rd(pz, MAGIC);
       const float wx = px - (tx - MAGIC), wy = py - (ty - MAGIC), wz = pz - (tz - MAGIC);
-      const int off = (__float_as_int(tx) - MAGIC_BITS) + (__float_as_int(ty) - MAGIC_BITS) * nxp +
+      const int off = (__float_as_int(tx) - MAGIC_BITS) * sx + (__float_as_int(ty) - MAGIC_BITS) * sy +
                       (__float_as_int(tz) - MAGIC_BITS) * nxyp;
       if (off != prev) {
         q0 = __ldg(cell + off);         // slice z:   x/x+1 at y, y+1
@@ -584,6 +594,34 @@ __global__ void pad_volume_kernel(const float* __restrict__ vol, float4* __restr
   }
 }
 
+// the y-fastest copy (FpArgs::vqT), written in its own order (coalesced stores)
+__global__ void pad_volume_t_kernel(const float* __restrict__ vol, float4* __restrict__ vqt, int nx,
+                                    int ny, int nz) {
+  const int nxp = nx + 4, nyp = ny + 4, nzp = nz + 4;
+  const long long total = (long long)nxp * nyp * nzp;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int py = int(i % nyp);
+    const long long r = i / nyp;
+    const int px = int(r % nxp), pz = int(r / nxp);
+    const int x = px - 2, y = py - 2, z = pz - 2;
+    float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (z >= 0 && z < nz) {
+      const float* s = vol + (long long)z * ny * nx;
+      const bool x0 = x >= 0 && x < nx, x1 = x + 1 >= 0 && x + 1 < nx;
+      if (y >= 0 && y < ny) {
+        if (x0) q.x = __ldg(s + (long long)y * nx + x);
+        if (x1) q.y = __ldg(s + (long long)y * nx + x + 1);
+      }
+      if (y + 1 >= 0 && y + 1 < ny) {
+        if (x0) q.z = __ldg(s + (long long)(y + 1) * nx + x);
+        if (x1) q.w = __ldg(s + (long long)(y + 1) * nx + x + 1);
+      }
+    }
+    vqt[i] = q;
+  }
+}
+
 }  // namespace cone
 }  // namespace tgb
 
@@ -613,6 +651,7 @@ struct tg_cone_plan {
   filt::RowFilter* ramlak = nullptr;
   // scratch
   float4* d_vpad = nullptr;  // K2 quad volume (zero border 2)
+  int k2_tu = 32;            // K2 CTA width in u (band height 256 / k2_tu rows)
   size_t vpad_elems = 0;
   float* d_pitched = nullptr;  // band copy with a 16-byte row pitch when n_u % 4 != 0
   size_t pitched_elems = 0;
@@ -794,7 +833,8 @@ void backproject_impl(tg_cone_plan& p, uint64_t z0, uint64_t nz, uint64_t v0, ui
 }
 
 void ensure_vpad(tg_cone_plan& p) {
-  const size_t need = size_t(p.vol.shape[0] + 4) * (p.vol.shape[1] + 4) * (p.vol.shape[2] + 4);
+  // x-fastest and y-fastest quad volumes back to back
+  const size_t need = 2 * size_t(p.vol.shape[0] + 4) * (p.vol.shape[1] + 4) * (p.vol.shape[2] + 4);
   if (p.vpad_elems >= need) return;
   if (p.d_vpad) TG_CUDA(cudaFree(p.d_vpad));
   TG_CUDA(cudaMalloc(&p.d_vpad, need * sizeof(float4)));
@@ -810,6 +850,8 @@ void forward_impl(tg_cone_plan& p, uint64_t view0, uint64_t nviews, const float*
   const int nx = int(p.vol.shape[0]), ny = int(p.vol.shape[1]), nz = int(p.vol.shape[2]);
   if (pad) {
     pad_volume_kernel<<<148 * 8, 256, 0, st>>>(d_vol, p.d_vpad, nx, ny, nz);
+    pad_volume_t_kernel<<<148 * 8, 256, 0, st>>>(d_vol, p.d_vpad + p.vpad_elems / 2, nx, ny, nz);
+    TG_LAUNCHED(1);
     TG_LAUNCHED(1);
   }
   FpArgs a;
@@ -830,6 +872,8 @@ void forward_impl(tg_cone_plan& p, uint64_t view0, uint64_t nviews, const float*
   a.step = 0.5 * m;
   a.geo = p.d_geo;
   a.vq = p.d_vpad;
+  a.vqT = p.d_vpad + p.vpad_elems / 2;
+  a.dual = env_int("TG_K2_DUAL", 1);  // experiment knob: 0 = x-fastest copy only
   a.nxp = nx + 4;
   a.nyp = ny + 4;
   KernelTimer timer;
@@ -839,8 +883,12 @@ void forward_impl(tg_cone_plan& p, uint64_t view0, uint64_t nviews, const float*
     const uint64_t cn = std::min<uint64_t>(65535, nviews - c0);
     a.view0 = int(view0 + c0);
     a.out = d_out + c0 * p.det.n_u * p.det.n_v;
-    dim3 grid((a.nu + 31) / 32, unsigned(cn), (a.nv + 7) / 8);
-    cone_fp_kernel<<<grid, 256, 0, st>>>(a);
+    const int TU = p.k2_tu;
+    dim3 grid((a.nu + TU - 1) / TU, unsigned(cn), (a.nv + 256 / TU - 1) / (256 / TU));
+    if (TU == 64)
+      cone_fp_kernel<64><<<grid, 256, 0, st>>>(a);
+    else
+      cone_fp_kernel<32><<<grid, 256, 0, st>>>(a);
     TG_LAUNCHED(1);
   }
   timer.stop();
@@ -1040,6 +1088,14 @@ tg_status tg_cone_plan_create(const tg_cone_geometry* g, int device, tg_cone_pla
     TG_CUDA(cudaMalloc(&p->d_geo, geo.size() * sizeof(double)));
     TG_CUDA(cudaMemcpy(p->d_geo, geo.data(), geo.size() * sizeof(double), cudaMemcpyHostToDevice));
     p->k1_k = default_k1_k();
+    // K2 band height: 8 detector rows (TU = 32) while a quad-volume slice is
+    // small; 4 rows (TU = 64) once a slice passes 8 MB, so the sheet of volume
+    // a band's rays cross stays L2-resident (c4 4.3 MB: 449 vs 459 ms;
+    // c5 16.9 MB: 4.52 vs 4.80 s)
+    {
+      const double slice_mb = double(g->volume.shape[0] + 4) * double(g->volume.shape[1] + 4) * 16.0 / 1e6;
+      p->k2_tu = env_int("TG_K2_TU", slice_mb >= 8.0 ? 64 : 32) == 64 ? 64 : 32;
+    }
     size_box(*p);
     *out = p.release();
   });
