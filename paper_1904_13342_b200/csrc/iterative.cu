@@ -21,6 +21,7 @@
 //    (x, grad in; x' out), neighbour re-reads hit L1/L2.
 #include <cmath>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -148,6 +149,22 @@ struct AsyncBuf {
   AsyncBuf& operator=(const AsyncBuf&) = delete;
 };
 
+// keep freed stream-ordered allocations cached in the device pool (the
+// default release threshold returns them to the driver at every sync, so each
+// loop call would re-map its multi-GB work buffers)
+inline void keep_pool(cudaStream_t st) {
+  static std::once_flag once[64];
+  int dev = 0;
+  TG_CUDA(cudaGetDevice(&dev));
+  std::call_once(once[dev & 63], [&] {
+    cudaMemPool_t pool;
+    TG_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+    uint64_t thr = ~0ull;
+    TG_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+  });
+  (void)st;
+}
+
 struct Scratch {
   AsyncBuf<double> buf;
   double* partial;
@@ -220,6 +237,7 @@ void tv_loop(Fwd fwd, Bwd bwd, uint64_t n_sino, uint64_t nx, uint64_t ny, uint64
              const float* d_sino, float* d_x, uint64_t iterations, double lr, double lambda,
              double* h_hist, cudaStream_t st) {
   const uint64_t n_vox = nx * ny * nz;
+  keep_pool(st);
   AsyncBuf<float> fp_b(n_sino, st), bp_b(n_vox, st), x2_b(n_vox, st);
   AsyncBuf<double> sums_b(2 * (iterations + 1), st);  // [iterations + 1][2] = (data, tv)
   float *fp = fp_b.p, *bp = bp_b.p, *x2 = x2_b.p;

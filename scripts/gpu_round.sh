@@ -28,6 +28,10 @@ for w in $WHAT; do
       timeout 1200 ncu --set full --clock-control none --import-source on -k regex:cone_bp_kernel \
         -s 3 -c 1 -o $OUT/${TAG}_k1 -f python bench.py --steps 3 --warmup 3 --fp-steps 1 \
         --no-cpu-baseline > $OUT/${TAG}_ncu_k1.log 2>&1 ;;
+    ncuk3)
+      timeout 900 ncu --set full --clock-control none --import-source on -k regex:filter_kernel \
+        -c 1 -o $OUT/${TAG}_k3 -f python bench.py --steps 3 --warmup 3 --fp-steps 1 \
+        --no-cpu-baseline --c5-iters 0 > $OUT/${TAG}_ncu_k3.log 2>&1 ;;
     ncufp)
       timeout 1500 ncu --set full --clock-control none --import-source on -k regex:cone_fp_kernel \
         -c 1 -o $OUT/${TAG}_k2 -f python bench.py --steps 3 --warmup 3 --fp-steps 1 \
