@@ -55,18 +55,52 @@ def env_rank():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled every 200 ms (B200_PROFILING.md)."""
+    """SM clock + throttle reasons sampled DURING the timed region
+    (B200_PROFILING.md clocks line): NVML every 10 ms on a thread, falling
+    back to `nvidia-smi -lms 200` when pynvml is unavailable."""
 
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, gpu_index):
         self.gpu = gpu_index
-        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.rows = []
+        self.nvml = None
         self.p = None
+        self.f = None
+
+    def _poll(self):
+        import pynvml as N
+        h = N.nvmlDeviceGetHandleByIndex(self.gpu)
+        mx = N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)
+        bits = {"hw_slowdown": N.nvmlClocksEventReasonHwSlowdown,
+                "hw_thermal_slowdown": N.nvmlClocksEventReasonHwThermalSlowdown,
+                "sw_thermal_slowdown": N.nvmlClocksEventReasonSwThermalSlowdown,
+                "sw_power_cap": N.nvmlClocksEventReasonSwPowerCap}
+        while not self._stop.is_set():
+            try:
+                sm = N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)
+                r = N.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.rows.append((float(sm), float(mx), [n for n, b in bits.items() if r & b]))
+            except Exception:
+                pass
+            self._stop.wait(0.01)
 
     def __enter__(self):
+        import threading
+        try:
+            import pynvml as N
+            N.nvmlInit()
+            self.nvml = N
+            self._stop = threading.Event()
+            self._t = threading.Thread(target=self._poll, daemon=True)
+            self._t.start()
+            return self
+        except Exception:
+            self.nvml = None
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
         try:
             self.p = subprocess.Popen(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}",
                                        "--format=csv,noheader,nounits", "-lms", "200"],
@@ -76,6 +110,10 @@ class ClockSampler:
         return self
 
     def __exit__(self, *a):
+        if self.nvml is not None:
+            self._stop.set()
+            self._t.join(timeout=2)
+            return
         if self.p is not None:
             self.p.terminate()
             try:
@@ -84,24 +122,23 @@ class ClockSampler:
                 self.p.kill()
 
     def summary(self):
-        if self.p is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.f.flush()
-        rows = []
-        with open(self.f.name) as f:
-            for line in f:
-                parts = [x.strip() for x in line.split(",")]
-                if len(parts) >= 9:
-                    rows.append(parts)
-        os.unlink(self.f.name)
-        if not rows:
+        if self.nvml is None:
+            if self.p is None:
+                return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+            self.f.flush()
+            with open(self.f.name) as f:
+                for line in f:
+                    parts = [x.strip() for x in line.split(",")]
+                    if len(parts) >= 9 and parts[1].replace(".", "").isdigit():
+                        rs = [n for n, v in zip(self.NAMES, parts[5:9]) if v.lower() == "active"]
+                        self.rows.append((float(parts[1]), float(parts[2]), rs))
+            os.unlink(self.f.name)
+        if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
-        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({n for r in rows for n, v in zip(names, r[5:9]) if v.lower() == "active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(rows)}
+        return {"sm_mhz": statistics.median(r[0] for r in self.rows),
+                "sm_max_mhz": max(r[1] for r in self.rows),
+                "reasons": sorted({n for r in self.rows for n in r[2]}),
+                "samples": len(self.rows), "source": "nvml 10 ms" if self.nvml else "nvidia-smi"}
 
 
 def c4_geometry(tg):
@@ -344,6 +381,18 @@ def main():
     e2e_h2d = int(h_band.numel() * 4) * world
     e2e_d2h = int(h_slab.numel() * 4) * world
     e2e_parity = float((h_slab.to(dev) * scale - slab).abs().max() / slab.abs().max().clamp_min(1e-30))
+    # PCIe copy rates on this box (pinned, one DMA each) to explain e2e
+    def copy_ms(dst, src):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        dst.copy_(src, non_blocking=True)
+        b.record(stream)
+        torch.cuda.synchronize()
+        return a.elapsed_time(b)
+    h2d_ms = copy_ms(band, h_band)
+    d2h_ms = copy_ms(h_slab, slab)
+    pcie = {"h2d_gbs": h_band.numel() * 4 / (h2d_ms / 1e3) / 1e9, "h2d_ms": h2d_ms,
+            "d2h_gbs": h_slab.numel() * 4 / (d2h_ms / 1e3) / 1e9, "d2h_ms": d2h_ms}
 
     # ---- roofline (K1) --------------------------------------------------------
     pk = peaks()
@@ -416,7 +465,8 @@ def main():
                     "h2d_bytes_per_step": e2e_h2d,
                     "d2h_bytes_per_step": e2e_d2h,
                     "path": "tg_cone_backproject_slab_host (pinned host band -> device, chunked "
-                            "H2D overlapped with K1, D2H of the slab)", "max_rel_diff_vs_device": e2e_parity},
+                            "H2D overlapped with K1, D2H of the slab)", "max_rel_diff_vs_device": e2e_parity,
+                    "ms_per_step": 1e3 * e2e_s / e2e_n, "pcie": pcie},
             "fp": {"metric": "cone forward projection Gsamples/s (c4, Shepp-Logan)",
                    "value": fp_value, "unit": "Gsamples/s", "ms": fp_ms, "samples": fp_samples,
                    "roofline": {"bound": "l1", "peak": l1_peak / 2, "frac": fp_value / (l1_peak / 2),

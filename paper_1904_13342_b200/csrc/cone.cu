@@ -983,7 +983,16 @@ void host_backproject(tg_cone_plan& p, uint64_t z0, uint64_t nz, uint64_t v0, ui
     d_band = ensure_buffer(p.d_stage_in, p.stage_in_elems, np * per_view);
     d_slab = ensure_buffer(p.d_stage_out, p.stage_out_elems, nvox);
   }
-  HostPipe hp(n_chunks);
+  // The device-to-host copy of the slab overlaps the last views' K1: the
+  // final two view chunks are back-projected z-part by z-part (32-aligned,
+  // so every K1 tile is the one the whole-slab launch would run) and each
+  // part leaves as soon as its last view is in.
+  const uint64_t plane = p.vol.shape[0] * p.vol.shape[1];
+  const bool split = n_chunks >= 3 && nz >= 64;
+  const int n_head = split ? n_chunks - 2 : n_chunks;
+  const uint64_t pz = split ? std::max<uint64_t>(32, (nz / 8 + 31) / 32 * 32) : nz;
+  const int n_parts = int((nz + pz - 1) / pz);
+  HostPipe hp(n_chunks + n_parts);
   const float scale = fdk ? float(fdk_scale(p, use_parker)) : 1.0f;
   for (int c = 0; c < n_chunks; ++c) {
     const uint64_t w0 = uint64_t(c) * chunk, wn = std::min(chunk, np - w0);
@@ -996,9 +1005,23 @@ void host_backproject(tg_cone_plan& p, uint64_t z0, uint64_t nz, uint64_t v0, ui
     TG_CUDA(cudaStreamWaitEvent(hp.cs, hp.ev[c], 0));
     float* part = d_band + w0 * per_view;
     if (fdk) prefilter_impl(p, part, part, use_parker, v0, n_rows, w0, wn, hp.cs);
-    backproject_impl(p, z0, nz, v0, n_rows, d_band, d_slab, scale, c > 0, hp.cs, w0, wn);
+    if (c < n_head) backproject_impl(p, z0, nz, v0, n_rows, d_band, d_slab, scale, c > 0, hp.cs, w0, wn);
   }
-  TG_CUDA(cudaMemcpyAsync(h_slab, d_slab, nvox * sizeof(float), cudaMemcpyDeviceToHost, hp.cs));
+  if (!split) {
+    TG_CUDA(cudaMemcpyAsync(h_slab, d_slab, nvox * sizeof(float), cudaMemcpyDeviceToHost, hp.cs));
+  } else {
+    const uint64_t w_tail = uint64_t(n_head) * chunk;
+    for (int q = 0; q < n_parts; ++q) {
+      const uint64_t zq = uint64_t(q) * pz, nq = std::min(pz, nz - zq);
+      backproject_impl(p, z0 + zq, nq, v0, n_rows, d_band, d_slab + zq * plane, scale, 1, hp.cs,
+                       w_tail, np - w_tail);
+      TG_CUDA(cudaEventRecord(hp.ev[n_chunks + q], hp.cs));
+      TG_CUDA(cudaStreamWaitEvent(hp.xs, hp.ev[n_chunks + q], 0));
+      TG_CUDA(cudaMemcpyAsync(h_slab + zq * plane, d_slab + zq * plane, nq * plane * sizeof(float),
+                              cudaMemcpyDeviceToHost, hp.xs));
+    }
+    TG_CUDA(cudaStreamSynchronize(hp.xs));
+  }
   TG_CUDA(cudaStreamSynchronize(hp.cs));
 }
 
