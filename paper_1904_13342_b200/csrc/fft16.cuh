@@ -127,7 +127,7 @@ __device__ __forceinline__ float preweight(float v, const PreWeights& pw, uint64
 
 // One Stockham radix-R pass (Bainville): butterfly j reads src[j + r P/R],
 // twiddles by w_P(r k P/(Ns R)) with k = j mod Ns, writes dst[(j-k) R + k + r Ns].
-template <int P, int R, bool INV, int SRC, int DST>
+template <int P, int R, bool INV, int SRC, int DST, bool PW = true>
 __device__ __forceinline__ void pass(const float2* __restrict__ x, float2* __restrict__ y, int Ns,
                                      const float2* __restrict__ tw, const RowIO& io) {
   constexpr int NB = P / R;          // butterflies
@@ -144,8 +144,13 @@ __device__ __forceinline__ void pass(const float2* __restrict__ x, float2* __res
       if constexpr (SRC == SRC_GLOBAL) {
         float2 z = make_float2(0.f, 0.f);
         if (i < io.n) {
-          z.x = preweight(io.pa[i], io.pw, io.ra, i, io.n);
-          if (io.pb) z.y = preweight(io.pb[i], io.pw, io.ra + 1, i, io.n);
+          if (PW) {
+            z.x = preweight(io.pa[i], io.pw, io.ra, i, io.n);
+            if (io.pb) z.y = preweight(io.pb[i], io.pw, io.ra + 1, i, io.n);
+          } else {
+            z.x = io.pa[i];
+            if (io.pb) z.y = io.pb[i];
+          }
         }
         v[r] = z;
       } else {
@@ -198,14 +203,16 @@ __host__ __device__ constexpr int tw_table_size() {
   return P == 8192 ? 256 + 16 * 256 + 2 * 4096 : 256 + (P / 256) * 256;
 }
 
-// occupancy target: 16 resident warps per SM (<= 128 registers per thread)
-template <int P>
+// occupancy target: 16 resident warps per SM (<= 128 registers per thread);
+// without fused pre-weights the P = 4096 transform fits 3 CTAs (24 warps)
+template <int P, bool PW>
 constexpr int min_blocks() {
-  return (512 / (P / 16)) < 1 ? 1 : ((512 / (P / 16)) > 16 ? 16 : (512 / (P / 16)));
+  return (!PW && P == 4096) ? 2
+                            : ((512 / (P / 16)) < 1 ? 1 : ((512 / (P / 16)) > 16 ? 16 : (512 / (P / 16))));
 }
 
-template <int P>
-__global__ void __launch_bounds__(P / 16, min_blocks<P>()) filter_kernel(const float* in, float* out, int n,
+template <int P, bool PW>
+__global__ void __launch_bounds__(P / 16, (min_blocks<P, PW>())) filter_kernel(const float* in, float* out, int n,
                                                         uint64_t n_rows, int packed,
                                                         const float* __restrict__ w,
                                                         const float2* __restrict__ tw,
@@ -227,7 +234,7 @@ __global__ void __launch_bounds__(P / 16, min_blocks<P>()) filter_kernel(const f
   io.out_scale = 1.0f / float(P);
   constexpr int RL = (P == 8192) ? 2 : P / 256;  // last radix
   // forward
-  pass<P, 16, false, SRC_GLOBAL, DST_SMEM>(nullptr, A, 1, tw, io);
+  pass<P, 16, false, SRC_GLOBAL, DST_SMEM, PW>(nullptr, A, 1, tw, io);
   __syncthreads();
   if constexpr (P == 8192) {
     pass<P, 16, false, SRC_SMEM, DST_SMEM>(A, B, 16, tw + tw_offset<P>(16), io);

@@ -188,6 +188,17 @@ void destroy(RowFilter* f) {
   delete f;
 }
 
+// FDK pre-weights as one elementwise pass: row r of the launch, bin j
+__global__ void __launch_bounds__(256) preweight_kernel(const float* in, float* out, uint64_t total,
+                                                        int n, PreWeights pw) {
+  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t row = i / uint64_t(n);
+    const int j = int(i - row * uint64_t(n));
+    out[i] = pre_weight(in[i], pw, row, j, n);
+  }
+}
+
 void apply(const RowFilter& f, const float* d_in, float* d_out, uint64_t n_rows,
            const PreWeights* pw, cudaStream_t st) {
   if (n_rows == 0) return;
@@ -199,17 +210,30 @@ void apply(const RowFilter& f, const float* d_in, float* d_out, uint64_t n_rows,
   KernelTimer timer;
   timer.start(st);
   const int n = int(f.n);
+  // The FP64 cosine / Parker pre-weights run as their own elementwise pass
+  // (HBM-bound, exact double products rounded to fp32 per map) so the FFT
+  // kernel keeps its registers for the transform (P = 4096: 3 CTAs / SM).
+  const bool sep = (w.cos || w.parker) && f.P >= 512 && f.P <= 8192;
+  const float* src = d_in;
+  if (sep) {
+    const uint64_t total = n_rows * f.n;
+    const unsigned pb = unsigned(std::min<uint64_t>((total + 255) / 256, 148ull * 16));
+    preweight_kernel<<<pb, 256, 0, st>>>(d_in, d_out, total, n, w);
+    TG_LAUNCHED(1);
+    src = d_out;
+    w = PreWeights{};
+  }
   auto launch16 = [&](auto kern, int P, size_t smem) {
     TG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    kern<<<unsigned(blocks), P / 16, smem, st>>>(d_in, d_out, n, n_rows, int(packed), f.d_w, f.d_tw16,
+    kern<<<unsigned(blocks), P / 16, smem, st>>>(src, d_out, n, n_rows, int(packed), f.d_w, f.d_tw16,
                                                   w);
   };
   switch (f.P) {
-    case 512: launch16(fft16::filter_kernel<512>, 512, fft16::smem_bytes<512>()); break;
-    case 1024: launch16(fft16::filter_kernel<1024>, 1024, fft16::smem_bytes<1024>()); break;
-    case 2048: launch16(fft16::filter_kernel<2048>, 2048, fft16::smem_bytes<2048>()); break;
-    case 4096: launch16(fft16::filter_kernel<4096>, 4096, fft16::smem_bytes<4096>()); break;
-    case 8192: launch16(fft16::filter_kernel<8192>, 8192, fft16::smem_bytes<8192>()); break;
+    case 512: launch16(fft16::filter_kernel<512, false>, 512, fft16::smem_bytes<512>()); break;
+    case 1024: launch16(fft16::filter_kernel<1024, false>, 1024, fft16::smem_bytes<1024>()); break;
+    case 2048: launch16(fft16::filter_kernel<2048, false>, 2048, fft16::smem_bytes<2048>()); break;
+    case 4096: launch16(fft16::filter_kernel<4096, false>, 4096, fft16::smem_bytes<4096>()); break;
+    case 8192: launch16(fft16::filter_kernel<8192, false>, 8192, fft16::smem_bytes<8192>()); break;
     default: {  // small windows: generic radix-4 shared-memory transform
       const size_t smem = 2 * f.P * sizeof(float2);
       TG_CUDA(cudaFuncSetAttribute(row_filter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
