@@ -188,6 +188,35 @@ __device__ __forceinline__ void pass(const float2* __restrict__ x, float2* __res
   }
 }
 
+// P = 4096 middle: the forward's last radix-16 pass (span 256) leaves thread
+// j holding X[j + 256 r], r = 0..15 — exactly the inputs of the inverse's
+// first pass (span 1, no twiddles).  Filter multiply and the inverse DFT16
+// therefore run in registers: one shared-memory round trip and one barrier
+// fewer per row pair.
+template <int P>
+__device__ __forceinline__ void fused_middle(const float2* __restrict__ x, float2* __restrict__ y,
+                                             const float2* __restrict__ tw, const float* __restrict__ w) {
+  static_assert(P == 4096, "fused middle pass is specific to P = 4096 (radix 16^3)");
+  constexpr int NB = P / 16;
+  const int j = threadIdx.x;  // one butterfly per thread (k = j for span 256)
+  float2 v[16];
+#pragma unroll
+  for (int r = 0; r < 16; ++r) v[r] = x[pad(j + r * NB)];
+#pragma unroll
+  for (int r = 1; r < 16; ++r) v[r] = cmul(v[r], __ldg(tw + r * 256 + j));
+  dft<16, false>(v);
+  float2 u[16];
+#pragma unroll
+  for (int r = 0; r < 16; ++r) {
+    const float wk = __ldg(w + j + r * NB);
+    const float2 xr = v[slot<16>(r)];
+    u[r] = make_float2(xr.x * wk, xr.y * wk);
+  }
+  dft<16, true>(u);
+#pragma unroll
+  for (int r = 0; r < 16; ++r) y[pad(j * 16 + r)] = u[slot<16>(r)];
+}
+
 // offset of the twiddle table of the pass with span Ns (Ns = 16, 256, 4096)
 template <int P>
 __host__ __device__ constexpr int tw_offset(int Ns) {
@@ -251,6 +280,14 @@ __global__ void __launch_bounds__(P / 16, (min_blocks<P, PW>())) filter_kernel(c
     pass<P, 16, true, SRC_SMEM, DST_SMEM>(B, A, 256, tw + tw_offset<P>(256), io);
     __syncthreads();
     pass<P, 2, true, SRC_SMEM, DST_GLOBAL>(A, nullptr, 4096, tw + tw_offset<P>(4096), io);
+  } else if constexpr (P == 4096) {
+    pass<P, 16, false, SRC_SMEM, DST_SMEM>(A, B, 16, tw + tw_offset<P>(16), io);
+    __syncthreads();
+    fused_middle<P>(B, A, tw + tw_offset<P>(256), w);  // fwd pass 3, filter, inv pass 1
+    __syncthreads();
+    pass<P, 16, true, SRC_SMEM, DST_SMEM>(A, B, 16, tw + tw_offset<P>(16), io);
+    __syncthreads();
+    pass<P, RL, true, SRC_SMEM, DST_GLOBAL>(B, nullptr, 256, tw + tw_offset<P>(256), io);
   } else {
     pass<P, 16, false, SRC_SMEM, DST_SMEM>(A, B, 16, tw + tw_offset<P>(16), io);
     __syncthreads();
