@@ -127,7 +127,11 @@ __device__ __forceinline__ float preweight(float v, const PreWeights& pw, uint64
 
 // One Stockham radix-R pass (Bainville): butterfly j reads src[j + r P/R],
 // twiddles by w_P(r k P/(Ns R)) with k = j mod Ns, writes dst[(j-k) R + k + r Ns].
-template <int P, int R, bool INV, int SRC, int DST, bool PW = true>
+// HALF: the row occupies at most the first P/2 samples (P >= 2 n, always
+// true for the FDK window next_pow2(2 n)): in the first pass inputs r >= R/2
+// are zero and in the last pass outputs r >= R/2 are discarded, so the
+// compiler prunes that half of the butterfly arithmetic.
+template <int P, int R, bool INV, int SRC, int DST, bool PW = true, bool HALF = false>
 __device__ __forceinline__ void pass(const float2* __restrict__ x, float2* __restrict__ y, int Ns,
                                      const float2* __restrict__ tw, const RowIO& io) {
   constexpr int NB = P / R;          // butterflies
@@ -143,7 +147,7 @@ __device__ __forceinline__ void pass(const float2* __restrict__ x, float2* __res
       const int i = j + r * NB;
       if constexpr (SRC == SRC_GLOBAL) {
         float2 z = make_float2(0.f, 0.f);
-        if (i < io.n) {
+        if ((!HALF || r < R / 2) && i < io.n) {
           if (PW) {
             z.x = preweight(io.pa[i], io.pw, io.ra, i, io.n);
             if (io.pb) z.y = preweight(io.pb[i], io.pw, io.ra + 1, i, io.n);
@@ -174,7 +178,7 @@ __device__ __forceinline__ void pass(const float2* __restrict__ x, float2* __res
       const int i = o + r * Ns;
       const float2 x_r = v[slot<R>(r)];
       if constexpr (DST == DST_GLOBAL) {
-        if (i < io.n) {
+        if ((!HALF || r < R / 2) && i < io.n) {
           io.oa[i] = x_r.x * io.out_scale;
           if (io.ob) io.ob[i] = x_r.y * io.out_scale;
         }
@@ -240,7 +244,7 @@ constexpr int min_blocks() {
                             : ((512 / (P / 16)) < 1 ? 1 : ((512 / (P / 16)) > 16 ? 16 : (512 / (P / 16))));
 }
 
-template <int P, bool PW>
+template <int P, bool PW, bool HALF>
 __global__ void __launch_bounds__(P / 16, (min_blocks<P, PW>())) filter_kernel(const float* in, float* out, int n,
                                                         uint64_t n_rows, int packed,
                                                         const float* __restrict__ w,
@@ -263,7 +267,7 @@ __global__ void __launch_bounds__(P / 16, (min_blocks<P, PW>())) filter_kernel(c
   io.out_scale = 1.0f / float(P);
   constexpr int RL = (P == 8192) ? 2 : P / 256;  // last radix
   // forward
-  pass<P, 16, false, SRC_GLOBAL, DST_SMEM, PW>(nullptr, A, 1, tw, io);
+  pass<P, 16, false, SRC_GLOBAL, DST_SMEM, PW, HALF>(nullptr, A, 1, tw, io);
   __syncthreads();
   if constexpr (P == 8192) {
     pass<P, 16, false, SRC_SMEM, DST_SMEM>(A, B, 16, tw + tw_offset<P>(16), io);
@@ -287,7 +291,7 @@ __global__ void __launch_bounds__(P / 16, (min_blocks<P, PW>())) filter_kernel(c
     __syncthreads();
     pass<P, 16, true, SRC_SMEM, DST_SMEM>(A, B, 16, tw + tw_offset<P>(16), io);
     __syncthreads();
-    pass<P, RL, true, SRC_SMEM, DST_GLOBAL>(B, nullptr, 256, tw + tw_offset<P>(256), io);
+    pass<P, RL, true, SRC_SMEM, DST_GLOBAL, true, HALF>(B, nullptr, 256, tw + tw_offset<P>(256), io);
   } else {
     pass<P, 16, false, SRC_SMEM, DST_SMEM>(A, B, 16, tw + tw_offset<P>(16), io);
     __syncthreads();

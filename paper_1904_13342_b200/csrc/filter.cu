@@ -228,12 +228,21 @@ void apply(const RowFilter& f, const float* d_in, float* d_out, uint64_t n_rows,
     kern<<<unsigned(blocks), P / 16, smem, st>>>(src, d_out, n, n_rows, int(packed), f.d_w, f.d_tw16,
                                                   w);
   };
+  const bool half = 2 * f.n <= f.P;  // the row fills at most half the window
+#define TG_LAUNCH16(PP)                                                                   \
+  case PP:                                                                                \
+    if (half)                                                                             \
+      launch16(fft16::filter_kernel<PP, false, true>, PP, fft16::smem_bytes<PP>());       \
+    else                                                                                  \
+      launch16(fft16::filter_kernel<PP, false, false>, PP, fft16::smem_bytes<PP>());      \
+    break;
   switch (f.P) {
-    case 512: launch16(fft16::filter_kernel<512, false>, 512, fft16::smem_bytes<512>()); break;
-    case 1024: launch16(fft16::filter_kernel<1024, false>, 1024, fft16::smem_bytes<1024>()); break;
-    case 2048: launch16(fft16::filter_kernel<2048, false>, 2048, fft16::smem_bytes<2048>()); break;
-    case 4096: launch16(fft16::filter_kernel<4096, false>, 4096, fft16::smem_bytes<4096>()); break;
-    case 8192: launch16(fft16::filter_kernel<8192, false>, 8192, fft16::smem_bytes<8192>()); break;
+    TG_LAUNCH16(512)
+    TG_LAUNCH16(1024)
+    TG_LAUNCH16(2048)
+    TG_LAUNCH16(4096)
+    TG_LAUNCH16(8192)
+#undef TG_LAUNCH16
     default: {  // small windows: generic radix-4 shared-memory transform
       const size_t smem = 2 * f.P * sizeof(float2);
       TG_CUDA(cudaFuncSetAttribute(row_filter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
