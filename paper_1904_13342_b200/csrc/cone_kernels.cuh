@@ -42,7 +42,6 @@ struct BpArgs {
   // -(0x4B400000 * 4 * BOXU) mod 2^32: the magic-floor bias of a row address,
   // passed at run time so ptxas cannot split it back out of the per-view base
   uint32_t magic_row_off;
-  int lanemap;              // consumer warp shape: 1 = 8 x 4 (default, fewest bank conflicts), 0 = 16 x 2, 2 = 4 x 8
   const float* sino;        // band buffer (slow path gathers)
   long long row_pitch;      // elements between detector rows
   long long view_pitch;     // elements between views

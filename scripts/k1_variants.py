@@ -1,4 +1,7 @@
-"""Time K1 at c4 under the current TG_K1_* environment (one variant per
+"""[Experiment record: the TG_K1_BOXU / TG_K1_LANEMAP / TG_K2_TU / TG_K2_WU /
+TG_K2_DUAL knobs were removed from the library once the measurements in
+DESIGN.md §5 picked the winners; TG_K1_K remains.]
+Time K1 at c4 under the current TG_K1_* environment (one variant per
 process; the plan reads the knobs at creation).  Prints one JSON line.
 
     TG_K1_BOXU=52 TG_K1_LANEMAP=1 python scripts/k1_variants.py

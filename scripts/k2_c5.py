@@ -1,4 +1,7 @@
-"""Time K2 at config c5 (1024^3, 720 x [2048 x 1536]) under the current TG_K2_* env."""
+"""[Experiment record: the TG_K1_BOXU / TG_K1_LANEMAP / TG_K2_TU / TG_K2_WU /
+TG_K2_DUAL knobs were removed from the library once the measurements in
+DESIGN.md §5 picked the winners; TG_K1_K remains.]
+Time K2 at config c5 (1024^3, 720 x [2048 x 1536]) under the current TG_K2_* env."""
 import json
 import math
 import os

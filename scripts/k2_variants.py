@@ -1,4 +1,7 @@
-"""Time K2 (cone forward projection) at c4 under the current TG_K2_* env (one
+"""[Experiment record: the TG_K1_BOXU / TG_K1_LANEMAP / TG_K2_TU / TG_K2_WU /
+TG_K2_DUAL knobs were removed from the library once the measurements in
+DESIGN.md §5 picked the winners; TG_K1_K remains.]
+Time K2 (cone forward projection) at c4 under the current TG_K2_* env (one
 variant per process).  --sweep runs each variant in a subprocess."""
 import json
 import os

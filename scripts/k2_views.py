@@ -1,4 +1,7 @@
-"""K2 time per chunk of views (c4 or c5) under the current TG_K2_* env."""
+"""[Experiment record: the TG_K1_BOXU / TG_K1_LANEMAP / TG_K2_TU / TG_K2_WU /
+TG_K2_DUAL knobs were removed from the library once the measurements in
+DESIGN.md §5 picked the winners; TG_K1_K remains.]
+K2 time per chunk of views (c4 or c5) under the current TG_K2_* env."""
 import json
 import math
 import os
