@@ -418,6 +418,9 @@ def main():
             # SURVEY §8d's graded interpolation bound (TMU rate: 4 bilinear/clk/SM);
             # the smem-lerp kernel is not limited by it and exceeds it
             "graded_interp_gups": interp_peak, "graded_interp_frac": per_gpu_gups / interp_peak,
+            # scripts/tex_bench.cu on this pool's B200 (profiles/r1_tex_microbench.txt):
+            # tex2D fp32 bilinear fetches measured at 1161 G/s = 3.99 / clk / SM
+            "tex2d_bilinear_measured_gfetch_s": 1161.0,
             "hbm_peak_gbs": pk.get("hbm_gbs"),
             "hbm_compulsory_frac": (hbm_bytes / (k1_avg / 1e3) / 1e9) / float(pk.get("hbm_gbs", 6545.9))},
     }
