@@ -22,7 +22,7 @@ namespace cone {
 constexpr int BX = 16, BY = 16;
 constexpr int NCONS = BX * BY;          // consumer threads (8 warps)
 constexpr int NTHREADS = NCONS + 32;    // + one producer warp
-constexpr int STAGES = 8;               // projection boxes in flight
+constexpr int STAGES = 6;               // projection boxes in flight
 constexpr int kMaxConstViews = 640;     // FP64 matrices per constant-bank upload (60 KB)
 constexpr int MODE_FAST = 0, MODE_SLOW = 1, MODE_SKIP = 2;
 
