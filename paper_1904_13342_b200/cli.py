@@ -20,7 +20,6 @@ pipelines.hpp:191-261) is not part of the projector path and reports so.
 from __future__ import annotations
 
 import argparse
-import math
 import sys
 from typing import List
 

@@ -15,7 +15,6 @@ K9 fused TV + descent); only the loss history returns to the host.
 """
 from __future__ import annotations
 
-import ctypes as C
 from dataclasses import dataclass, field
 from typing import List, Tuple
 

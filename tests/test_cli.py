@@ -4,7 +4,6 @@ cli.hpp contract: exit codes 0 / 1 (usage) / 2 (data or processing error,
 subcommands end to end on the GPU with byte-identical outputs run to run
 (acceptance.cpp:486-548) and equal to the in-memory API."""
 import json
-import math
 import os
 
 import numpy as np
