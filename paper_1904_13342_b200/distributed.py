@@ -294,11 +294,14 @@ class PeerBuffers:
                 self._opened.append(p.value)
             self.peer.append(ptrs)
 
-    def close(self):
+    def close(self, group=None):
+        """Unmap the peers' buffers, wait until every rank has, then free our own
+        (an exporter must outlive every importer's mapping)."""
         L = N.lib()
         for p in self._opened:
             L.tg_ipc_close_handle(p)
         self._opened = []
+        dist.barrier(group=group)
         for p in self.own:
             L.tg_device_free(p)
         self.own = []
@@ -397,4 +400,4 @@ def tv_reconstruct_p2p(geo: ConeGeometry, p_part: torch.Tensor, iterations: int,
         return x, hist
     finally:
         sync_all()
-        bufs.close()
+        bufs.close(group)
