@@ -188,14 +188,35 @@ void destroy(RowFilter* f) {
   delete f;
 }
 
-// FDK pre-weights as one elementwise pass: row r of the launch, bin j
-__global__ void __launch_bounds__(256) preweight_kernel(const float* in, float* out, uint64_t total,
-                                                        int n, PreWeights pw) {
-  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
-       i += uint64_t(gridDim.x) * blockDim.x) {
-    const uint64_t row = i / uint64_t(n);
-    const int j = int(i - row * uint64_t(n));
-    out[i] = pre_weight(in[i], pw, row, j, n);
+// FDK pre-weights as one elementwise pass: one CTA per detector row (no
+// per-element index division), float4 loads / stores when rows are 16-byte
+// aligned; the FP64 products and their two fp32 roundings are the
+// reference's (filtering.hpp:136-154, applied cosine then Parker)
+__global__ void __launch_bounds__(256) preweight_kernel(const float* in, float* out, int n,
+                                                        PreWeights pw) {
+  const uint64_t row = blockIdx.x;
+  const float* src = in + row * uint64_t(n);
+  float* dst = out + row * uint64_t(n);
+  const double* cw = pw.cos ? pw.cos + (pw.cos_row0 + row % pw.rows_per_view) * uint64_t(n) : nullptr;
+  const double* pk = pw.parker ? pw.parker + (row / pw.rows_per_view) * uint64_t(n) : nullptr;
+  auto weigh = [&](float v, int j) {
+    if (cw) v = float(double(v) * __ldg(cw + j));
+    if (pk) v = float(double(v) * __ldg(pk + j));
+    return v;
+  };
+  if ((n & 3) == 0 && (reinterpret_cast<uintptr_t>(src) & 15) == 0 &&
+      (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+    for (int c = threadIdx.x; c < n / 4; c += blockDim.x) {
+      float4 v = reinterpret_cast<const float4*>(src)[c];
+      const int j = 4 * c;
+      v.x = weigh(v.x, j);
+      v.y = weigh(v.y, j + 1);
+      v.z = weigh(v.z, j + 2);
+      v.w = weigh(v.w, j + 3);
+      reinterpret_cast<float4*>(dst)[c] = v;
+    }
+  } else {
+    for (int j = threadIdx.x; j < n; j += blockDim.x) dst[j] = weigh(src[j], j);
   }
 }
 
@@ -216,9 +237,8 @@ void apply(const RowFilter& f, const float* d_in, float* d_out, uint64_t n_rows,
   const bool sep = (w.cos || w.parker) && f.P >= 512 && f.P <= 8192;
   const float* src = d_in;
   if (sep) {
-    const uint64_t total = n_rows * f.n;
-    const unsigned pb = unsigned(std::min<uint64_t>((total + 255) / 256, 148ull * 16));
-    preweight_kernel<<<pb, 256, 0, st>>>(d_in, d_out, total, n, w);
+    check(n_rows <= 2147483647ull, "too many detector rows for one filter launch");
+    preweight_kernel<<<unsigned(n_rows), 256, 0, st>>>(d_in, d_out, n, w);
     TG_LAUNCHED(1);
     src = d_out;
     w = PreWeights{};
