@@ -474,8 +474,13 @@ def main():
                    "value": fp_value, "unit": "Gsamples/s", "ms": fp_ms, "samples": fp_samples,
                    "roofline": {"bound": "l1", "peak": l1_peak / 2, "frac": fp_value / (l1_peak / 2),
                                 "note": "32 B of taps (two 16-B quad gathers) per trilinear sample"},
-                   "graded_interp_frac": fp_value / (interp_peak / 2), "graded_interp_peak": interp_peak / 2},
+                   "graded_interp_frac": fp_value / (interp_peak / 2), "graded_interp_peak": interp_peak / 2,
+                   # scripts/k2_tex_bench.cu: the same gather pattern with ideal coherence
+                   "measured_gather_ceiling_gsamples": 611.0,
+                   "measured_gather_ceiling_frac": fp_value / 611.0},
             "k3_fdk_prefilter_ms": k3_ms, "k1_ms_mean": k1_avg, "k1_ms_min": min(k1_ms),
+            # FDK of this rank's slab (pipelines.hpp:73-84): K3 on the band + K1
+            "fdk_ms": k3_ms + k1_avg,
             "roofline": roofline, "clocks": clocks, "gpu_launches": gpu_launches,
             "cpu_baseline": cpu,
             "c5_tv": c5,
