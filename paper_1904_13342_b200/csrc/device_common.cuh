@@ -70,7 +70,15 @@ struct ConstBank {
       owner[dev] = plan_id;
     }
   }
-  void release(int dev, cudaStream_t stream) { TG_CUDA(cudaEventRecord(last[dev], stream)); }
+  // Inside a CUDA-graph capture the owner cannot change (callers capture
+  // only work whose bank upload happened before the capture), so the
+  // ordering event is not recorded there.
+  void release(int dev, cudaStream_t stream) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    TG_CUDA(cudaStreamIsCapturing(stream, &cs));
+    if (cs == cudaStreamCaptureStatusActive) return;
+    TG_CUDA(cudaEventRecord(last[dev], stream));
+  }
   void forget(uint64_t plan_id) {
     std::lock_guard<std::mutex> lk(mu);
     for (auto& o : owner)

@@ -232,41 +232,100 @@ void tv_step(const float* x, const float* grad, const OutList& outs, uint64_t nx
 // One device-resident descent loop over any projector pair (fwd, bwd) —
 // pipelines.hpp:276-298 with the graph's evaluation order: forward (loss of
 // the current x), backward, step; a final forward records the last loss.
+// appends the (data, tv) pair of the step just finished to sums[] at a
+// device-side counter, so a captured iteration needs no per-step parameters
+__global__ void record_kernel(const double* __restrict__ slot, double* __restrict__ sums,
+                              int* __restrict__ counter) {
+  const int c = counter[0];
+  sums[2 * c] = slot[0];
+  sums[2 * c + 1] = slot[1];
+  counter[0] = c + 1;
+}
+
+// One device-resident descent loop over any projector pair (fwd, bwd) —
+// pipelines.hpp:276-298 with the graph's evaluation order: forward (loss of
+// the current x), backward, step; a final forward records the last loss.
+// graph_ok: the pair may be captured into a CUDA graph (no constant-bank
+// switches inside an iteration); small problems are launch-bound, so two
+// iterations (x -> x2 -> x) are captured once and replayed.
 template <typename Fwd, typename Bwd>
 void tv_loop(Fwd fwd, Bwd bwd, uint64_t n_sino, uint64_t nx, uint64_t ny, uint64_t nz,
              const float* d_sino, float* d_x, uint64_t iterations, double lr, double lambda,
-             double* h_hist, cudaStream_t st) {
+             double* h_hist, cudaStream_t st, bool graph_ok = false) {
   const uint64_t n_vox = nx * ny * nz;
   keep_pool(st);
   AsyncBuf<float> fp_b(n_sino, st), bp_b(n_vox, st), x2_b(n_vox, st);
   AsyncBuf<double> sums_b(2 * (iterations + 1), st);  // [iterations + 1][2] = (data, tv)
+  AsyncBuf<double> slot_b(2, st);
+  AsyncBuf<int> ctr_b(1, st);
+  TG_CUDA(cudaMemsetAsync(ctr_b.p, 0, sizeof(int), st));
   float *fp = fp_b.p, *bp = bp_b.p, *x2 = x2_b.p;
-  double* sums = sums_b.p;
+  double *sums = sums_b.p, *slot = slot_b.p;
+  int* ctr = ctr_b.p;
   Scratch sc(st);
+  auto step = [&](float* cur, float* nxt, cudaStream_t s) {
+    fwd(cur, fp, s);
+    l2_residual(fp, d_sino, fp, n_sino, slot, s, sc);
+    bwd(fp, bp, s);
+    tv_step(cur, bp, one_out(nxt), nx, ny, nz, 0, 0, lambda, lr, slot + 1, s, sc);
+    record_kernel<<<1, 1, 0, s>>>(slot, sums, ctr);
+    TG_LAUNCHED(1);
+  };
   float* cur = d_x;
   float* nxt = x2;
-  for (uint64_t it = 0; it < iterations; ++it) {
-    fwd(cur, fp);
-    l2_residual(fp, d_sino, fp, n_sino, sums + 2 * it, st, sc);
-    bwd(fp, bp);
-    tv_step(cur, bp, one_out(nxt), nx, ny, nz, 0, 0, lambda, lr, sums + 2 * it + 1, st, sc);
+  uint64_t it = 0;
+  if (graph_ok && iterations >= 5) {
+    step(cur, nxt, st);  // plan state (pads, constant bank owner) settles un-captured
+    std::swap(cur, nxt);
+    ++it;
+    // capture on a private stream (the caller's may be the legacy default)
+    cudaStream_t gs;
+    cudaEvent_t ev;
+    TG_CUDA(cudaStreamCreateWithFlags(&gs, cudaStreamNonBlocking));
+    TG_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    TG_CUDA(cudaEventRecord(ev, st));
+    TG_CUDA(cudaStreamWaitEvent(gs, ev, 0));
+    const uint64_t launches0 = tg_kernel_launch_count();
+    TG_CUDA(cudaStreamBeginCapture(gs, cudaStreamCaptureModeThreadLocal));
+    step(cur, nxt, gs);
+    step(nxt, cur, gs);
+    cudaGraph_t g;
+    TG_CUDA(cudaStreamEndCapture(gs, &g));
+    const uint64_t per_replay = tg_kernel_launch_count() - launches0;
+    cudaGraphExec_t ge;
+    TG_CUDA(cudaGraphInstantiate(&ge, g, 0));
+    const uint64_t replays = (iterations - it) / 2;
+    for (uint64_t r = 0; r < replays; ++r) TG_CUDA(cudaGraphLaunch(ge, gs));
+    count_launch(per_replay * (replays ? replays - 1 : 0));  // capture counted one replay's worth
+    it += 2 * replays;
+    TG_CUDA(cudaEventRecord(ev, gs));
+    TG_CUDA(cudaStreamWaitEvent(st, ev, 0));
+    TG_CUDA(cudaStreamSynchronize(gs));
+    cudaGraphExecDestroy(ge);
+    cudaGraphDestroy(g);
+    cudaEventDestroy(ev);
+    cudaStreamDestroy(gs);
+  }
+  for (; it < iterations; ++it) {
+    step(cur, nxt, st);
     std::swap(cur, nxt);
   }
-  fwd(cur, fp);
-  l2_residual(fp, d_sino, nullptr, n_sino, sums + 2 * iterations, st, sc);
-  tv_step(cur, nullptr, one_out(nullptr), nx, ny, nz, 0, 0, lambda, lr, sums + 2 * iterations + 1,
-          st, sc);
+  fwd(cur, fp, st);
+  l2_residual(fp, d_sino, nullptr, n_sino, slot, st, sc);
+  tv_step(cur, nullptr, one_out(nullptr), nx, ny, nz, 0, 0, lambda, lr, slot + 1, st, sc);
+  record_kernel<<<1, 1, 0, st>>>(slot, sums, ctr);
+  TG_LAUNCHED(1);
   if (cur != d_x)
     TG_CUDA(cudaMemcpyAsync(d_x, cur, n_vox * sizeof(float), cudaMemcpyDeviceToDevice, st));
   std::vector<double> s(2 * (iterations + 1));
   TG_CUDA(cudaMemcpyAsync(s.data(), sums, s.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
   TG_CUDA(cudaStreamSynchronize(st));
-  for (uint64_t it = 0; it <= iterations; ++it) {
+  for (uint64_t i = 0; i <= iterations; ++i) {
     // graph add node: data + (tv * lambda)   (graph.hpp:331-343)
-    const double loss = s[2 * it] + s[2 * it + 1] * lambda;
-    if (h_hist) h_hist[it] = loss;
+    const double loss = s[2 * i] + s[2 * i + 1] * lambda;
+    if (h_hist) h_hist[i] = loss;
     if (!std::isfinite(loss))
-      throw RefError("optimization diverged at iteration " + std::to_string(it) +
+      throw RefError("optimization diverged at iteration " + std::to_string(i) +
                      " (loss is not finite); lower the learning rate");
   }
 }
@@ -396,8 +455,11 @@ tg_status tg_cone_tv_reconstruct(tg_cone_plan* plan, const float* d_sino, float*
     auto ok = [](tg_status s) {
       if (s != TG_OK) throw RefError(tg_last_error());
     };
-    iter::tv_loop([&](const float* x, float* s) { ok(tg_cone_forward(plan, x, s, st)); },
-                  [&](const float* s, float* x) { ok(tg_cone_backproject(plan, s, x, 1.0f, 0, st)); },
+    iter::tv_loop(
+        [&](const float* x, float* s, cudaStream_t q) { ok(tg_cone_forward(plan, x, s, q)); },
+        [&](const float* s, float* x, cudaStream_t q) {
+          ok(tg_cone_backproject(plan, s, x, 1.0f, 0, q));
+        },
                   n_proj * det.n_u * det.n_v, vol.shape[0], vol.shape[1], vol.shape[2], d_sino,
                   d_x, iterations, learning_rate, tv_lambda, h_loss_history, st);
   });
@@ -415,11 +477,15 @@ tg_status tg_planar_tv_reconstruct(tg_planar_plan* plan, const float* d_sino, fl
     auto ok = [](tg_status s) {
       if (s != TG_OK) throw RefError(tg_last_error());
     };
+    // the planar pair is graph-capturable while its view table fits one
+    // constant-bank upload (K6 chunks of 2048 views)
     iter::tv_loop(
-        [&](const float* x, float* s) { ok(tg_planar_forward(plan, x, s, st)); },
-        [&](const float* s, float* x) { ok(tg_planar_backproject(plan, s, x, 1.0f, 0, st)); },
+        [&](const float* x, float* s, cudaStream_t q) { ok(tg_planar_forward(plan, x, s, q)); },
+        [&](const float* s, float* x, cudaStream_t q) {
+          ok(tg_planar_backproject(plan, s, x, 1.0f, 0, q));
+        },
         n_proj * det.n_bins, vol.shape[0], vol.shape[1], 1, d_sino, d_x, iterations,
-        learning_rate, tv_lambda, h_loss_history, st);
+        learning_rate, tv_lambda, h_loss_history, st, n_proj <= 2048);
   });
 }
 
