@@ -110,6 +110,11 @@ def tv_reconstruct(sino: Sinogram, geo, cfg: ExperimentConfig,
     cfg.learning_rate; returns the image and the iterations + 1 losses.
     Raises the reference's "optimization diverged ..." Error on a non-finite
     loss."""
+    if isinstance(geo, ConeGeometry):
+        _check_cone_sino(sino, geo)
+    else:
+        check(isinstance(geo, (ParallelGeometry, FanGeometry)), "unknown geometry type")
+        _check_planar_sino(sino, geo)
     data = require_f32(sino.data, "sinogram data")
     on_host = is_host(data)
     if on_host:
@@ -122,11 +127,8 @@ def tv_reconstruct(sino: Sinogram, geo, cfg: ExperimentConfig,
     args = (data.data_ptr(), x.data_ptr(), int(cfg.iterations), float(cfg.learning_rate),
             float(cfg.tv_lambda), hist.ctypes.data_as(N.c_dblp), stream_of(data))
     if isinstance(geo, ConeGeometry):
-        _check_cone_sino(sino, geo)
         N.check(L.tg_cone_tv_reconstruct(geo._plan(_dev(data)), *args))
     else:
-        check(isinstance(geo, (ParallelGeometry, FanGeometry)), "unknown geometry type")
-        _check_planar_sino(sino, geo)
         N.check(L.tg_planar_tv_reconstruct(geo._plan(_dev(data)), *args))
     img = Image(geo.volume, x.cpu().numpy() if on_host else x)
     return img, hist.tolist()
