@@ -287,6 +287,13 @@ tg_status tg_cone_tv_reconstruct(tg_cone_plan* plan, const float* d_sino, float*
 tg_status tg_planar_tv_reconstruct(tg_planar_plan* plan, const float* d_sino, float* d_x,
                                    uint64_t iterations, double learning_rate, double tv_lambda,
                                    double* h_loss_history, void* stream);
+/* the same with host buffers (h_x: initial image in, result out) */
+tg_status tg_cone_tv_reconstruct_host(tg_cone_plan* plan, const float* h_sino, float* h_x,
+                                      uint64_t iterations, double learning_rate, double tv_lambda,
+                                      double* h_loss_history);
+tg_status tg_planar_tv_reconstruct_host(tg_planar_plan* plan, const float* h_sino, float* h_x,
+                                        uint64_t iterations, double learning_rate,
+                                        double tv_lambda, double* h_loss_history);
 /* pipelines.hpp:119-132 add_gaussian_noise (host, bit-exact: std::mt19937_64
  * Box-Muller of pipelines.hpp:90-115; sigma = relative_std * max(in)) */
 tg_status tg_add_gaussian_noise(const float* h_in, float* h_out, uint64_t n, double relative_std,

@@ -291,5 +291,43 @@ Image<T> fdk_reconstruct(const Sinogram<T>& sino, const ConeGeometry& geo, bool 
   return img;
 }
 
+// pipelines.hpp:273-299 tv_reconstruct (x -> forward_project -> l2_loss(., p)
+// + tv_lambda * tv_loss(x), plain gradient descent from zero) with the whole
+// loop device resident: projections, l2 residual, TV subgradient and the
+// descent step never leave HBM; only the loss history returns.  Any
+// geometry type (the reference's graph nodes take all three).  The config
+// type is the caller's ExperimentConfig (learning_rate, iterations,
+// tv_lambda), so this header stays independent of pipelines.hpp.
+template <typename T, typename Geo, typename Cfg>
+std::pair<Image<T>, std::vector<double>> tv_reconstruct(const Sinogram<T>& sino, const Geo& geo,
+                                                        const Cfg& cfg) {
+  Image<T> img(geo.volume);
+  std::vector<double> hist(cfg.iterations + 1);
+  F32In<T> in(sino.data);
+  std::vector<float> x(img.data.size(), 0.0f);
+  const std::size_t nvox = x.size();
+  if constexpr (std::is_same_v<Geo, ConeGeometry>) {
+    check(sino.is_cone() && sino.n_projections == geo.n_projections &&
+              sino.detector2d.n_u == geo.detector.n_u && sino.detector2d.n_v == geo.detector.n_v,
+          "sinogram shape does not match the geometry");
+    throw_if(tg_cone_tv_reconstruct_host(cone_plan(geo).get(), in.p, x.data(), cfg.iterations,
+                                         cfg.learning_rate, cfg.tv_lambda, hist.data()));
+  } else {
+    check(!sino.is_cone() && sino.n_projections == geo.n_projections &&
+              sino.detector1d.n_bins == geo.detector.n_bins,
+          "sinogram shape does not match the geometry");
+    double sid = 0.0, sdd = 0.0;
+    if constexpr (std::is_same_v<Geo, FanGeometry>) {
+      sid = geo.sid;
+      sdd = geo.sdd;
+    }
+    throw_if(tg_planar_tv_reconstruct_host(planar_plan(geo, sid, sdd).get(), in.p, x.data(),
+                                           cfg.iterations, cfg.learning_rate, cfg.tv_lambda,
+                                           hist.data()));
+  }
+  for (std::size_t i = 0; i < nvox; ++i) img.data[i] = T(x[i]);
+  return {std::move(img), std::move(hist)};
+}
+
 }  // namespace b200
 }  // namespace tomograd

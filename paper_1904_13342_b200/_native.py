@@ -120,6 +120,8 @@ SIGNATURES = {
     "tg_ipc_close_handle": (c_int, [c_vp]),
     "tg_cone_tv_reconstruct": (c_int, [c_vp, c_vp, c_vp, c_u64, c_dbl, c_dbl, c_dblp, c_vp]),
     "tg_planar_tv_reconstruct": (c_int, [c_vp, c_vp, c_vp, c_u64, c_dbl, c_dbl, c_dblp, c_vp]),
+    "tg_cone_tv_reconstruct_host": (c_int, [c_vp, c_vp, c_vp, c_u64, c_dbl, c_dbl, c_dblp]),
+    "tg_planar_tv_reconstruct_host": (c_int, [c_vp, c_vp, c_vp, c_u64, c_dbl, c_dbl, c_dblp]),
     "tg_add_gaussian_noise": (c_int, [c_vp, c_vp, c_u64, c_dbl, c_u64]),
     "tg_kernel_launch_count": (c_u64, []),
     "tg_set_timing": (None, [c_int]),

@@ -330,6 +330,32 @@ void tv_loop(Fwd fwd, Bwd bwd, uint64_t n_sino, uint64_t nx, uint64_t ny, uint64
   }
 }
 
+// host-buffer forms of the loop: one upload, the device loop, one download
+template <typename Run>
+tg_status tv_host(int device, uint64_t n_sino, uint64_t n_vox, const float* h_sino, float* h_x,
+                  Run run) {
+  return guarded([&] {
+    DeviceGuard dg(device);
+    cudaStream_t st;
+    TG_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    tg_status r = TG_OK;
+    std::string msg;
+    {
+      AsyncBuf<float> s(n_sino, st), x(n_vox, st);
+      TG_CUDA(cudaMemcpyAsync(s.p, h_sino, n_sino * sizeof(float), cudaMemcpyHostToDevice, st));
+      TG_CUDA(cudaMemcpyAsync(x.p, h_x, n_vox * sizeof(float), cudaMemcpyHostToDevice, st));
+      r = run(s.p, x.p, st);
+      if (r == TG_OK)
+        TG_CUDA(cudaMemcpyAsync(h_x, x.p, n_vox * sizeof(float), cudaMemcpyDeviceToHost, st));
+      else
+        msg = tg_last_error();
+    }  // stream-ordered frees enqueued before the stream goes away
+    TG_CUDA(cudaStreamSynchronize(st));
+    cudaStreamDestroy(st);
+    if (r != TG_OK) throw RefError(msg);
+  });
+}
+
 }  // namespace iter
 }  // namespace tgb
 
@@ -404,6 +430,40 @@ tg_status tg_l2_residual_scatter(const float* d_fp, const float* d_p, uint64_t n
     iter::sum_partials_kernel<<<1, iter::kRedThreads, 0, st>>>(sc.partial, iter::kRedBlocks, d_sum);
     TG_LAUNCHED(2);
   });
+}
+
+tg_status tg_cone_tv_reconstruct_host(tg_cone_plan* plan, const float* h_sino, float* h_x,
+                                      uint64_t iterations, double learning_rate, double tv_lambda,
+                                      double* h_loss_history) {
+  tg_volume_spec vol;
+  tg_detector2d det;
+  uint64_t n_proj = 0;
+  const tg_status s0 = tg_cone_plan_shape(plan, &vol, &det, &n_proj);
+  if (s0 != TG_OK) return s0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return iter::tv_host(dev, n_proj * det.n_u * det.n_v, vol.shape[0] * vol.shape[1] * vol.shape[2],
+                 h_sino, h_x, [&](const float* s, float* x, cudaStream_t st) {
+                   return tg_cone_tv_reconstruct(plan, s, x, iterations, learning_rate, tv_lambda,
+                                                 h_loss_history, st);
+                 });
+}
+
+tg_status tg_planar_tv_reconstruct_host(tg_planar_plan* plan, const float* h_sino, float* h_x,
+                                        uint64_t iterations, double learning_rate,
+                                        double tv_lambda, double* h_loss_history) {
+  tg_volume_spec vol;
+  tg_detector1d det;
+  uint64_t n_proj = 0;
+  const tg_status s0 = tg_planar_plan_shape(plan, &vol, &det, &n_proj);
+  if (s0 != TG_OK) return s0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return iter::tv_host(dev, n_proj * det.n_bins, vol.shape[0] * vol.shape[1], h_sino, h_x,
+                 [&](const float* s, float* x, cudaStream_t st) {
+                   return tg_planar_tv_reconstruct(plan, s, x, iterations, learning_rate,
+                                                   tv_lambda, h_loss_history, st);
+                 });
 }
 
 // ---- peer memory (CUDA IPC) for the fused multi-GPU exchanges -------------

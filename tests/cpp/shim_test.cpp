@@ -168,6 +168,22 @@ int main() {
     auto [img, hist] = tv_reconstruct(s3, g3, cfg);
     report("reference graph tv_reconstruct on B200 operators", hist.back() < hist.front(),
            "loss " + std::to_string(hist.front()) + " -> " + std::to_string(hist.back()));
+    // the whole loop on the device (b200::tv_reconstruct) against the oracle's
+    // FP64 restatement of the same loop (bitwise the reference's graph)
+    auto [img2, hist2] = b200::tv_reconstruct(s3, g3, cfg);
+    or_volume o3 = ov(v3);
+    std::vector<double> rays;
+    for (const auto& r : g3.rays) rays.insert(rays.end(), {r.x, r.y});
+    or_planar op{o3, {g3.detector.n_bins, g3.detector.spacing, g3.detector.origin}, g3.n_projections,
+                 g3.angular_range, 0.0, 0.0, rays.data(), g3.angles.data()};
+    std::vector<double> xo(img2.data.size(), 0.0), ho(cfg.iterations + 1);
+    or_tv_reconstruct_planar_f64(&op, s3.data.data(), xo.data(), cfg.iterations, cfg.learning_rate,
+                                 cfg.tv_lambda, ho.data());
+    double hmax = 0;
+    for (std::size_t i = 0; i < ho.size(); ++i) hmax = std::max(hmax, std::abs(hist2[i] - ho[i]) / ho[i]);
+    report("b200::tv_reconstruct loss history vs FP64 loop", hmax <= 5e-4,
+           "max_rel=" + std::to_string(hmax));
+    close("b200::tv_reconstruct image vs FP64 loop", rel_err(img2.data, xo), 1e-2, 5e-2);
   }
 
   // error text passes through unchanged
