@@ -362,24 +362,43 @@ __global__ void __maxnreg__(72)
           }
         }
       } else {
-        // general calibrated matrices: full projective map per voxel
+        // general calibrated matrices: the full projective map per voxel,
+        // voxels k and k + K/2 as FP32x2 pairs; the reciprocal is the MUFU
+        // approximation (~1 ulp: far inside the parity tolerance), the
+        // address takes the run-time magic bias like the circular path
+        constexpr int H = K / 2;
+        const uint32_t base2 = sbase + a.magic_row_off + 0u - MAGIC_BITS * 4u;
+        const float2 sz2 = make_float2(sz, sz), dz02 = make_float2(dz0, dz0);
+        const float2 Wz = make_float2(W.z, W.z), Uz = make_float2(U.z, U.z), Vz = make_float2(V.z, V.z);
+        const float2 hz02 = make_float2(hz0, hz0), un2 = make_float2(un, un), vn2 = make_float2(vn, vn);
+        const float2 sid22 = make_float2(a.sid2, a.sid2);
+        const float2 M2 = make_float2(MAGIC, MAGIC), nM2 = make_float2(-MAGIC, -MAGIC);
 #pragma unroll
-        for (int k = 0; k < K; ++k) {
-          const float dz = fmaf(float(min(k, kmax)), sz, dz0);
-          const float r = __frcp_rn(fmaf(W.z, dz, hz0));
-          const float u = fmaf(U.z, dz, un) * r;
-          const float vk = fmaf(V.z, dz, vn) * r;
-          const float tu = __fadd_rd(u, MAGIC);
-          const float tv = __fadd_rd(vk, MAGIC);
-          const float wu = u - (tu - MAGIC);
-          const float wv = vk - (tv - MAGIC);
-          const uint32_t ad = sbase + (__float_as_uint(tu) - MAGIC_BITS) * 4u +
-                              (__float_as_uint(tv) - MAGIC_BITS) * ROWB;
-          float a0, a1, b0, b1;
-          lds_quad<ROWB>(ad, a0, a1, b0, b1);
-          const float top = fmaf(wu, a1 - a0, a0);
-          const float bot = fmaf(wu, b1 - b0, b0);
-          ACC(k) = fmaf(fmaf(wv, bot - top, top), a.sid2 * r * r, ACC(k));
+        for (int k = 0; k < H; ++k) {
+          const float2 kk = make_float2(float(min(k, kmax)), float(min(k + H, kmax)));
+          const float2 dz = __ffma2_rn(kk, sz2, dz02);
+          const float2 hz = __ffma2_rn(Wz, dz, hz02);
+          float2 r;
+          asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r.x) : "f"(hz.x));
+          asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r.y) : "f"(hz.y));
+          const float2 u = __fmul2_rn(__ffma2_rn(Uz, dz, un2), r);
+          const float2 v = __fmul2_rn(__ffma2_rn(Vz, dz, vn2), r);
+          const float2 tu = __fadd2_rd(u, M2), tv = __fadd2_rd(v, M2);
+          const float2 fu = __fadd2_rn(tu, nM2), fv = __fadd2_rn(tv, nM2);
+          const float2 wu = __fadd2_rn(u, make_float2(-fu.x, -fu.y));
+          const float2 wv = __fadd2_rn(v, make_float2(-fv.x, -fv.y));
+          const float2 iw = __fmul2_rn(__fmul2_rn(sid22, r), r);
+          float a0, a1, b0, b1, c0, c1, d0, d1;
+          lds_quad<ROWB>(mad_u32<ROWB>(__float_as_uint(tv.x), base2 + __float_as_uint(tu.x) * 4u),
+                         a0, a1, b0, b1);
+          lds_quad<ROWB>(mad_u32<ROWB>(__float_as_uint(tv.y), base2 + __float_as_uint(tu.y) * 4u),
+                         c0, c1, d0, d1);
+          const float2 p0 = make_float2(a0, c0), p1 = make_float2(a1, c1);
+          const float2 q0 = make_float2(b0, d0), q1 = make_float2(b1, d1);
+          const float2 top = __ffma2_rn(wu, __fadd2_rn(p1, make_float2(-p0.x, -p0.y)), p0);
+          const float2 bot = __ffma2_rn(wu, __fadd2_rn(q1, make_float2(-q0.x, -q0.y)), q0);
+          const float2 mid = __ffma2_rn(wv, __fadd2_rn(bot, make_float2(-top.x, -top.y)), top);
+          acc[k] = __ffma2_rn(mid, iw, acc[k]);
         }
       }
     } else if (mode == MODE_SLOW) {
