@@ -303,7 +303,9 @@ __global__ void __maxnreg__(CIRC ? 72 : 96)
       if (CIRC) {
         // P[0][2] == P[2][2] == 0: u and 1/w^2 are constant along z and v is
         // affine in z (SURVEY §7 hard part (b)).
-        const float r = __frcp_rn(hz0);
+        // MUFU reciprocal (~1 ulp; no IEEE slow path in the per-view prologue)
+        float r;
+        asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(hz0));
         const float invw2 = a.sid2 * r * r;
         const float u = un * r;
         const float fu = floorf(u);
