@@ -537,7 +537,7 @@ __global__ void __launch_bounds__(256, 4) cone_fp_kernel(const FpArgs a) {
   const double ddx = dt * d[0] / a.sx, ddy = dt * d[1] / a.sy, ddz = dt * d[2] / a.sz;
   const float fdx = float(ddx), fdy = float(ddy), fdz = float(ddz);
   const int nxyp = a.nxp * a.nyp;
-  const bool xdom = fabs(d[0]) > fabs(d[1]);
+  const bool xdom = a.vqT != nullptr && fabs(d[0]) > fabs(d[1]);
   const float4* vbase = xdom ? a.vqT : a.vq;
   const int sx = xdom ? a.nyp : 1, sy = xdom ? 1 : a.nxp;
   constexpr float MAGIC = 12582912.0f;  // 1.5 * 2^23: t = M + floor(p) under round-down
@@ -668,6 +668,7 @@ struct tg_cone_plan {
   filt::RowFilter* ramlak = nullptr;
   // scratch
   float4* d_vpad = nullptr;  // K2 quad volume (zero border 2)
+  bool k2_dual = true;       // y-fastest copy present (memory permitting)
   int k2_tu = 32;            // K2 CTA width in u (band height 256 / k2_tu rows)
   size_t vpad_elems = 0;
   float* d_pitched = nullptr;  // band copy with a 16-byte row pitch when n_u % 4 != 0
@@ -842,10 +843,18 @@ void backproject_impl(tg_cone_plan& p, uint64_t z0, uint64_t nz, uint64_t v0, ui
 }
 
 void ensure_vpad(tg_cone_plan& p) {
-  // x-fastest and y-fastest quad volumes back to back
-  const size_t need = 2 * size_t(p.vol.shape[0] + 4) * (p.vol.shape[1] + 4) * (p.vol.shape[2] + 4);
-  if (p.vpad_elems >= need) return;
+  // x-fastest and y-fastest quad volumes back to back (8.8x the volume); when
+  // that does not fit next to the caller's data (volumes beyond ~1200^3 on a
+  // 180 GB B200) fall back to the x-fastest copy alone (4.4x)
+  const size_t one = size_t(p.vol.shape[0] + 4) * (p.vol.shape[1] + 4) * (p.vol.shape[2] + 4);
+  if (p.vpad_elems >= one * (p.k2_dual ? 2 : 1)) return;
   if (p.d_vpad) TG_CUDA(cudaFree(p.d_vpad));
+  p.d_vpad = nullptr;
+  p.vpad_elems = 0;
+  size_t free_b = 0, total_b = 0;
+  TG_CUDA(cudaMemGetInfo(&free_b, &total_b));
+  p.k2_dual = 2 * one * sizeof(float4) + total_b / 20 <= free_b;
+  const size_t need = one * (p.k2_dual ? 2 : 1);
   TG_CUDA(cudaMalloc(&p.d_vpad, need * sizeof(float4)));
   p.vpad_elems = need;
 }
@@ -859,8 +868,10 @@ void forward_impl(tg_cone_plan& p, uint64_t view0, uint64_t nviews, const float*
   const int nx = int(p.vol.shape[0]), ny = int(p.vol.shape[1]), nz = int(p.vol.shape[2]);
   if (pad) {
     pad_volume_kernel<<<148 * 8, 256, 0, st>>>(d_vol, p.d_vpad, nx, ny, nz);
-    pad_volume_t_kernel<<<148 * 8, 256, 0, st>>>(d_vol, p.d_vpad + p.vpad_elems / 2, nx, ny, nz);
-    TG_LAUNCHED(1);
+    if (p.k2_dual) {
+      pad_volume_t_kernel<<<148 * 8, 256, 0, st>>>(d_vol, p.d_vpad + p.vpad_elems / 2, nx, ny, nz);
+      TG_LAUNCHED(1);
+    }
     TG_LAUNCHED(1);
   }
   FpArgs a;
@@ -881,7 +892,7 @@ void forward_impl(tg_cone_plan& p, uint64_t view0, uint64_t nviews, const float*
   a.step = 0.5 * m;
   a.geo = p.d_geo;
   a.vq = p.d_vpad;
-  a.vqT = p.d_vpad + p.vpad_elems / 2;
+  a.vqT = p.k2_dual ? p.d_vpad + p.vpad_elems / 2 : nullptr;
   a.nxp = nx + 4;
   a.nyp = ny + 4;
   KernelTimer timer;

@@ -65,3 +65,29 @@ def test_accumulate_adds_to_existing(tg, O):
                                         torch.cuda.current_stream().cuda_stream))
     want = base.cpu().numpy().astype(np.float64) + 0.5 * O.cone_backproject(og, s).astype(np.float64)
     assert_close(out.cpu().numpy(), want, what="accumulate")
+
+
+def test_k2_single_layout_fallback_is_bitwise_equal(tg, O):
+    """When the x- and y-fastest quad volumes do not both fit, K2 falls back
+    to the x-fastest copy alone: same samples, same arithmetic, same bits."""
+    import gc
+    vol = tg.VolumeSpec.centered([96, 88, 80], [1.0] * 3)
+    det = tg.Detector2D.centered(120, 100, 1.2, 1.2)
+    ph = tg.shepp_logan_3d(vol, device=DEV)
+    geo_a = tg.make_cone(vol, det, 40, 2 * math.pi, 300.0, 600.0)
+    want = tg.forward_project(ph, geo_a).data.clone()
+    one = 100 * 92 * 84 * 16  # one quad layout, bytes
+    torch.cuda.synchronize()
+    free, _ = torch.cuda.mem_get_info()
+    total = torch.cuda.get_device_properties(0).total_memory
+    # leave room for one layout (+ margins) but not two
+    hog = torch.empty(int(free - total // 20 - int(1.5 * one) - (256 << 20)), dtype=torch.uint8,
+                      device=DEV)
+    try:
+        geo_b = tg.make_cone(vol, det, 40, 2 * math.pi, 300.0, 600.0)  # fresh plan
+        got = tg.forward_project(ph, geo_b).data.clone()
+    finally:
+        del hog
+        gc.collect()
+        torch.cuda.empty_cache()
+    assert torch.equal(got, want)
