@@ -230,11 +230,13 @@ def tv_reconstruct_sharded(geo: ConeGeometry, p_part: torch.Tensor, iterations: 
         last = it == iterations
         data = ops.residual(fp, p_part, None if last else fp)
         if last:
-            tv = ops.tv_step(x, me, None, None, tv_lambda, learning_rate)
+            tv = ops.tv_step(x, me, None, None, tv_lambda, learning_rate) if me.nz else 0.0
         else:
             band = exchange_bands(fp, views, shards, rank, group)
-            ops.backproject_slab(band, me, bp)
-            tv = ops.tv_step(x, me, bp, xs, tv_lambda, learning_rate)
+            tv = 0.0
+            if me.nz:  # more ranks than 32-slice slabs: this rank only projects
+                ops.backproject_slab(band, me, bp)
+                tv = ops.tv_step(x, me, bp, xs, tv_lambda, learning_rate)
         d, t = sum_in_rank_order([data, tv], p_part.device, group)
         loss = d + t * tv_lambda
         hist.append(loss)
@@ -361,20 +363,22 @@ def tv_reconstruct_p2p(geo: ConeGeometry, p_part: torch.Tensor, iterations: int,
             d_tv = sums.data_ptr() + 8 * (2 * it + 1)
             if last:
                 N.check(L.tg_l2_residual(fp.data_ptr(), p_part.data_ptr(), None, fp.numel(), d_sum, st))
-                N.check(L.tg_tv_step(x_own + 4 * me.z0 * plane, None, None, nx, ny, me.nz,
-                                     int(me.z0 > 0), int(me.z0 + me.nz < nz), float(tv_lambda),
-                                     float(learning_rate), d_tv, st))
+                if me.nz:
+                    N.check(L.tg_tv_step(x_own + 4 * me.z0 * plane, None, None, nx, ny, me.nz,
+                                         int(me.z0 > 0), int(me.z0 + me.nz < nz), float(tv_lambda),
+                                         float(learning_rate), d_tv, st))
                 break
             N.check(L.tg_l2_residual_scatter(fp.data_ptr(), p_part.data_ptr(), vwn, nv, nu, vw0,
                                              dests, world, d_sum, st))
             sync_all()  # every band complete
-            N.check(L.tg_cone_backproject_slab(plan, me.z0, me.nz, me.v0, me.n_rows, band,
-                                               bp.data_ptr(), 1.0, 0, st))
-            outs = (C.c_void_p * world)(*[bufs.peer[r][nxt] + 4 * me.z0 * plane
-                                          for r in range(world)])
-            N.check(L.tg_tv_step_multi(x_own + 4 * me.z0 * plane, bp.data_ptr(), outs, world, nx,
-                                       ny, me.nz, int(me.z0 > 0), int(me.z0 + me.nz < nz),
-                                       float(tv_lambda), float(learning_rate), d_tv, st))
+            if me.nz:  # more ranks than 32-slice slabs: this rank only projects
+                N.check(L.tg_cone_backproject_slab(plan, me.z0, me.nz, me.v0, me.n_rows, band,
+                                                   bp.data_ptr(), 1.0, 0, st))
+                outs = (C.c_void_p * world)(*[bufs.peer[r][nxt] + 4 * me.z0 * plane
+                                              for r in range(world)])
+                N.check(L.tg_tv_step_multi(x_own + 4 * me.z0 * plane, bp.data_ptr(), outs, world,
+                                           nx, ny, me.nz, int(me.z0 > 0), int(me.z0 + me.nz < nz),
+                                           float(tv_lambda), float(learning_rate), d_tv, st))
             sync_all()  # every slab in every next replica
             cur, nxt = nxt, cur
         # loss partials of all ranks, summed in rank order

@@ -75,7 +75,7 @@ def _setup(O):
     return geo, og, sino
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, align=1):
     import sys
     sys.path.insert(0, ROOT)
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
@@ -88,21 +88,23 @@ def _worker(rank, world, port, q):
         geo, og, sino = _setup(O)
         v0, vn = D.view_partition(geo, world)[rank]
         p = torch.from_numpy(np.ascontiguousarray(sino[v0:v0 + vn]))
-        x, hist = D.tv_reconstruct_sharded(geo, p, ITERS, LR, LAM, ops=OracleTvOps(O, og), align=1)
+        x, hist = D.tv_reconstruct_sharded(geo, p, ITERS, LR, LAM, ops=OracleTvOps(O, og),
+                                           align=align)
         q.put((rank, x.numpy(), hist))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [1, 2, 3])
-def test_sharded_tv_loop_bitwise_vs_single_process(world):
+@pytest.mark.parametrize("world,align", [(1, 1), (2, 1), (3, 1), (3, 16)])
+def test_sharded_tv_loop_bitwise_vs_single_process(world, align):
+    """(3, 16): slabs of 16, 8 and 0 slices — the last rank only projects"""
     import sys
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import oracle as O
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, align)) for r in range(world)]
     for p in procs:
         p.start()
     got = [q.get(timeout=240) for _ in range(world)]
