@@ -294,6 +294,41 @@ tg_status tg_cone_tv_reconstruct_host(tg_cone_plan* plan, const float* h_sino, f
 tg_status tg_planar_tv_reconstruct_host(tg_planar_plan* plan, const float* h_sino, float* h_x,
                                         uint64_t iterations, double learning_rate,
                                         double tv_lambda, double* h_loss_history);
+/* ---- the remaining graph nodes on the device ---------
+ * The reference's reverse-mode graph (graph.hpp) over device fp32 values:
+ * forward_project / backproject nodes call the projector entry points above
+ * (their registered gradients are each other, graph.hpp:408-434, with
+ * accumulate = 1 for the back-projection); the rest are these.  Arithmetic is
+ * FP64 rounded once to fp32; reductions use fixed grids (deterministic). */
+/* add / scale nodes and gradient accumulation (graph.hpp:318-328, 498-508):
+ * out = alpha a + beta b; d_b NULL: out = alpha a.  out may alias a or b. */
+tg_status tg_axpby(const float* d_a, const float* d_b, float* d_out, uint64_t n, double alpha,
+                   double beta, void* stream);
+/* multiply_weights node (graph.hpp:137-149, 303-310): out[i] = x[i] w[i % block] */
+tg_status tg_multiply_weights(const float* d_x, const float* d_w, float* d_out, uint64_t n,
+                              uint64_t block, void* stream);
+/* its gradient (graph.hpp:449-460): gx[i] += g[i] w[i % block];
+ * gw[j] += sum over rows g x (either output may be NULL) */
+tg_status tg_multiply_weights_grad(const float* d_g, const float* d_x, const float* d_w, float* d_gx,
+                                   float* d_gw, uint64_t n, uint64_t block, void* stream);
+/* fourier_filter node (graph.hpp:152-164, 312-316, 386-401): each of n_rows
+ * rows of n samples zero-padded to P, Re(IFFT(k FFT(row))), first n kept; k is
+ * a device vector of P weights (any real values: a trainable parameter) */
+tg_status tg_fourier_filter(const float* d_x, const float* d_k, float* d_out, uint64_t n_rows,
+                            uint64_t n, uint64_t P, void* stream);
+/* its weight gradient (graph.hpp:478-496): gk[f] += sum_rows Re(X_f conj G_f) / P.
+ * (The input gradient is tg_fourier_filter of the upstream gradient.) */
+tg_status tg_fourier_filter_weight_grad(const float* d_x, const float* d_g, float* d_gk,
+                                        uint64_t n_rows, uint64_t n, uint64_t P, void* stream);
+/* l2_loss gradient (graph.hpp:498-509, upstream gs): d = 2 gs (a - b);
+ * ga += d; gb -= d (either may be NULL).  The value is tg_l2_residual. */
+tg_status tg_l2_grad(const float* d_a, const float* d_b, float* d_ga, float* d_gb, uint64_t n,
+                     double gs, void* stream);
+/* tv_loss gradient (graph.hpp:511-528, upstream gs) over an [nz][ny][nx]
+ * block: gx += gs * subgrad_TV(x); *d_tv = TV(x).  d_gx must not alias d_x. */
+tg_status tg_tv_grad(const float* d_x, float* d_gx, uint64_t nx, uint64_t ny, uint64_t nz,
+                     double gs, double* d_tv, void* stream);
+
 /* pipelines.hpp:119-132 add_gaussian_noise (host, bit-exact: std::mt19937_64
  * Box-Muller of pipelines.hpp:90-115; sigma = relative_std * max(in)) */
 tg_status tg_add_gaussian_noise(const float* h_in, float* h_out, uint64_t n, double relative_std,

@@ -649,6 +649,51 @@ class Ref:
         return out
 
 
+    @staticmethod
+    def learn_filter_graph(g: Planar, sino, P, lr, iterations):
+        """experiment_learn_filter's graph (pipelines.hpp:211-259) run by the
+        reference's own Graph on a given float64 sinogram."""
+        sino = np.ascontiguousarray(sino, dtype=np.float64)
+        it = int(iterations)
+        loss = np.zeros(it + 1); dist = np.zeros(it + 1); w = np.zeros(int(P))
+        rec = np.zeros(g.img_shape_yx)
+        s = g.struct()
+        Ref._chk(ref().ref_learn_filter_graph(C.byref(s), _ptr(sino), C.c_uint64(int(P)),
+                                              C.c_double(lr), C.c_uint64(it), _ptr(loss),
+                                              _ptr(dist), _ptr(w), _ptr(rec)))
+        return loss, dist, w, rec
+
+    @staticmethod
+    def experiment_learn_filter(g: Planar, phantom, noise, seed, window, lr, iterations):
+        """pipelines.hpp:196-261 itself; returns (loss, dist, weights, recon)."""
+        it = int(iterations)
+        P = int(window) if window else filter_window(int(g.det.n_bins))
+        loss = np.zeros(it + 1); dist = np.zeros(it + 1); w = np.zeros(P)
+        rec = np.zeros(g.img_shape_yx)
+        padded = C.c_uint64(0)
+        s = g.struct()
+        Ref._chk(ref().ref_experiment_learn_filter(
+            C.byref(s), phantom.encode(), C.c_double(noise), C.c_uint64(int(seed)),
+            C.c_uint64(int(window)), C.c_double(lr), C.c_uint64(it), _ptr(loss), _ptr(dist),
+            _ptr(w), _ptr(rec), C.byref(padded)))
+        assert padded.value == P
+        return loss, dist, w, rec
+
+    @staticmethod
+    def graph_probe(g: Planar, x0, w0, sino, lam):
+        """loss = l2(multiply_weights(forward_project(x), w), p) + scale(tv(x), lam):
+        the value and the gradients of x and w after one backward (reference Graph)."""
+        x0 = np.ascontiguousarray(x0, dtype=np.float64)
+        w0 = np.ascontiguousarray(w0, dtype=np.float64)
+        sino = np.ascontiguousarray(sino, dtype=np.float64)
+        loss = C.c_double(0.0)
+        gx = np.zeros(g.img_shape_yx); gw = np.zeros(int(g.det.n_bins))
+        s = g.struct()
+        Ref._chk(ref().ref_graph_probe(C.byref(s), int(g.fan), _ptr(x0), _ptr(w0), _ptr(sino),
+                                       C.c_double(lam), C.byref(loss), _ptr(gx), _ptr(gw)))
+        return loss.value, gx, gw
+
+
 def rel_errors(out: np.ndarray, ref_: np.ndarray):
     """(max|d| / max|ref|, relRMSE = ||d||2 / ||ref||2) — SURVEY §8c metrics."""
     d = out.astype(np.float64) - ref_.astype(np.float64)
@@ -735,3 +780,18 @@ def mt19937_64(seed, k) -> int:
     fn = lib().or_mt19937_64_first
     fn.restype = C.c_uint64
     return int(fn(C.c_uint64(int(seed)), C.c_uint64(int(k))))
+
+
+def learn_filter_planar(g: Planar, sino, P, lr, iterations):
+    """Restatement of experiment_learn_filter's graph loop (pipelines.hpp:211-259)
+    on storage sino.dtype; returns (loss, dist, weights, recon)."""
+    suf, ct = _typed(sino.dtype)
+    sino = np.ascontiguousarray(sino)
+    it = int(iterations)
+    loss = np.zeros(it + 1); dist = np.zeros(it + 1); w = np.zeros(int(P))
+    rec = np.zeros(g.img_shape_yx, dtype=sino.dtype)
+    s = g.struct()
+    _check(getattr(lib(), f"or_learn_filter_planar_{suf}")(
+        C.byref(s), _ptr(sino, ct), C.c_uint64(int(P)), C.c_double(lr), C.c_uint64(it),
+        _ptr(loss), _ptr(dist), _ptr(w), _ptr(rec, ct)))
+    return loss, dist, w, rec

@@ -7,7 +7,9 @@
 // Nothing here re-implements an algorithm: every call goes to the
 // reference's own functions.  Used only to pin the restatement (tests/) and
 // as bench.py's "reference" CPU arm.
+#include <cmath>
 #include <cstring>
+#include <numbers>
 #include <exception>
 #include <string>
 #include <vector>
@@ -111,9 +113,134 @@ std::vector<double> tv_graph(const Sinogram<>& sino, const Geo& geo, const Exper
   return history;
 }
 
+// pipelines.hpp:211-259 (experiment_learn_filter's graph and loop) on a
+// given sinogram: the same nodes, feeds, record and descent order, so the
+// device graph can be compared on an identical fp32 input.  Pinned against
+// the reference function itself by ref_experiment_learn_filter (tests).
+void learn_filter_graph(const Sinogram<>& sino, const ParallelGeometry& geo, std::size_t window,
+                        double lr, std::size_t iterations, std::vector<double>& loss_h,
+                        std::vector<double>& dist_h, std::vector<double>& weights,
+                        std::vector<double>& recon_out) {
+  const Filter1D ramp = ramp_filter(geo.detector.n_bins, geo.detector.spacing, window);
+  const Filter1D ramlak = ramlak_filter(geo.detector.n_bins, geo.detector.spacing, window);
+  const std::size_t padded = ramp.padded_n;
+  double gap = 0.0;
+  for (std::size_t k = 0; k < padded; ++k) {
+    const double d = ramp.weights[k] - ramlak.weights[k];
+    gap += d * d;
+  }
+  gap = std::sqrt(gap);
+  Image<> reference = fbp_reconstruct(sino, geo, ramlak);
+  Graph g;
+  const NodeId p = g.input(sino.shape());
+  const NodeId K = g.parameter(Tensor<>({padded}, ramp.weights), true);
+  const NodeId target = g.parameter(reference.tensor(), false);
+  const NodeId filtered = g.fourier_filter(p, K, padded);
+  const NodeId bp = g.backproject(filtered, geo);
+  const NodeId recon = g.scale(bp, std::numbers::pi / double(geo.n_projections));
+  const NodeId loss = g.l2_loss(recon, target);
+  const std::map<NodeId, Tensor<>> feeds{{p, sino.tensor()}};
+  auto record = [&] {
+    loss_h.push_back(g.value(loss).scalar_value());
+    double d2 = 0.0;
+    const auto& w = g.node(K).value.data;
+    for (std::size_t k = 0; k < padded; ++k) {
+      const double d = w[k] - ramlak.weights[k];
+      d2 += d * d;
+    }
+    dist_h.push_back(gap > 0.0 ? std::sqrt(d2) / gap : 0.0);
+  };
+  for (std::size_t it = 0; it < iterations; ++it) {
+    g.forward(feeds);
+    record();
+    const auto grads = g.backward(loss);
+    gradient_descent_step(g, grads, lr);
+  }
+  g.forward(feeds);
+  record();
+  weights = g.node(K).value.data;
+  recon_out = g.value(recon).data;
+}
+
 }  // namespace
 
 extern "C" {
+
+// the graph of experiment_learn_filter on a given sinogram (see above)
+int ref_learn_filter_graph(const or_planar* gp, const double* sino, uint64_t window, double lr,
+                           uint64_t iterations, double* loss_h, double* dist_h, double* weights,
+                           double* recon) {
+  return guard([&] {
+    const auto geo = to_parallel(*gp);
+    auto s = Sinogram<>::planar(geo.n_projections, geo.detector);
+    std::memcpy(s.data.data(), sino, sizeof(double) * s.data.size());
+    std::vector<double> l, d, w, r;
+    learn_filter_graph(s, geo, std::size_t(window), lr, std::size_t(iterations), l, d, w, r);
+    std::memcpy(loss_h, l.data(), sizeof(double) * l.size());
+    std::memcpy(dist_h, d.data(), sizeof(double) * d.size());
+    std::memcpy(weights, w.data(), sizeof(double) * w.size());
+    std::memcpy(recon, r.data(), sizeof(double) * r.size());
+  });
+}
+
+// pipelines.hpp:196-261 experiment_learn_filter itself (phantom by name)
+int ref_experiment_learn_filter(const or_planar* gp, const char* phantom, double noise,
+                                uint64_t seed, uint64_t window, double lr, uint64_t iterations,
+                                double* loss_h, double* dist_h, double* weights, double* recon,
+                                uint64_t* padded_out) {
+  return guard([&] {
+    const auto geo = to_parallel(*gp);
+    ExperimentConfig cfg;
+    cfg.phantom = phantom;
+    cfg.noise_relative_std = noise;
+    cfg.seed = seed;
+    cfg.filter_window = std::size_t(window);
+    cfg.learning_rate = lr;
+    cfg.iterations = std::size_t(iterations);
+    auto r = experiment_learn_filter(geo, cfg);
+    std::memcpy(loss_h, r.loss_history.data(), sizeof(double) * r.loss_history.size());
+    std::memcpy(dist_h, r.distance_history.data(), sizeof(double) * r.distance_history.size());
+    std::memcpy(weights, r.learned_weights.data(), sizeof(double) * r.learned_weights.size());
+    std::memcpy(recon, r.reconstruction.data.data(), sizeof(double) * r.reconstruction.data.size());
+    *padded_out = r.ramp_init.padded_n;
+  });
+}
+
+// One forward + backward of a graph exercising the node kinds that
+// experiment_learn_filter does not:
+//   loss = l2(multiply_weights(forward_project(x), w), p) + scale(tv(x), lambda)
+// Outputs the loss and the gradients of x (image) and w (row weights, n_bins).
+int ref_graph_probe(const or_planar* gp, int fan, const double* x0, const double* w0,
+                    const double* sino, double lambda, double* loss, double* gx, double* gw) {
+  return guard([&] {
+    Graph g;
+    auto run = [&](const auto& geo) {
+      std::size_t nvox = 1;
+      for (auto d : geo.volume.shape) nvox *= d;
+      const NodeId x =
+          g.parameter(Tensor<>(geo.volume.shape, std::vector<double>(x0, x0 + nvox)), true);
+      const NodeId w = g.parameter(Tensor<>({geo.detector.n_bins},
+                                            std::vector<double>(w0, w0 + geo.detector.n_bins)),
+                                   true);
+      auto s = Sinogram<>::planar(geo.n_projections, geo.detector);
+      const NodeId p = g.input(s.shape());
+      std::memcpy(s.data.data(), sino, sizeof(double) * s.data.size());
+      const NodeId fp = g.forward_project(x, geo);
+      const NodeId mw = g.multiply_weights(fp, w);
+      const NodeId data_term = g.l2_loss(mw, p);
+      const NodeId l = g.add(data_term, g.scale(g.tv_loss(x), lambda));
+      g.forward({{p, s.tensor()}});
+      *loss = g.value(l).scalar_value();
+      auto grads = g.backward(l);
+      std::memcpy(gx, grads[x].data.data(), sizeof(double) * grads[x].data.size());
+      std::memcpy(gw, grads[w].data.data(), sizeof(double) * grads[w].data.size());
+    };
+    if (fan)
+      run(to_fan(*gp));
+    else
+      run(to_parallel(*gp));
+  });
+}
 
 int ref_tv_reconstruct_parallel(const or_planar* g, const double* sino, double* x,
                                 uint64_t iterations, double lr, double lambda, double* hist) {

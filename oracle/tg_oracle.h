@@ -114,7 +114,10 @@ int or_make_cone(const or_det2* det, uint64_t n, double range, double sid, doubl
   int or_tv_reconstruct_planar_##SUF(const or_planar* g, const T* sino, T* x,              \
                                      uint64_t iters, double lr, double lambda, double* hist); \
   int or_add_gaussian_noise_##SUF(const T* in, T* out, uint64_t n, double relative_std,     \
-                                  uint64_t seed);
+                                  uint64_t seed);                                              \
+  int or_learn_filter_planar_##SUF(const or_planar* g, const T* sino, uint64_t P, double lr,  \
+                                   uint64_t iterations, double* loss_h, double* dist_h,       \
+                                   double* w_out, T* recon_out);
 OR_DECLARE_ITER(f32, float)
 OR_DECLARE_ITER(f64, double)
 #undef OR_DECLARE_ITER

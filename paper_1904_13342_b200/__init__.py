@@ -17,8 +17,12 @@ from .geometry import (ConeGeometry, Detector1D, Detector2D, FanGeometry,  # noq
                        projection_matrices_circular, view_angles)
 from .phantom import (disk_phantom, head_phantom_ellipses, head_phantom_ellipsoids,  # noqa: F401
                       rasterize, shepp_logan_2d, shepp_logan_3d)
-from .iterative import (ExperimentConfig, TvResult, add_gaussian_noise,  # noqa: F401
-                        experiment_iterative_tv, l2_residual, tv_reconstruct, tv_step)
+from .iterative import (ExperimentConfig, FilterLearningResult, TvResult,  # noqa: F401
+                        add_gaussian_noise, experiment_iterative_tv, experiment_learn_filter,
+                        l2_residual, learn_filter, tv_reconstruct, tv_step)
+from .graph import (BackProject, FourierFilter, ForwardProject, Graph, OpKind,  # noqa: F401
+                    back_project_op, forward_project_op, fourier_filter_op,
+                    gradient_descent_step)
 from .pipelines import (FilterKind, fbp_reconstruct, fdk_prefilter, fdk_reconstruct,  # noqa: F401
                         fdk_scale, make_filter)
 from .projector import (back_project, cone_backproject_slab, cone_forward_views,  # noqa: F401

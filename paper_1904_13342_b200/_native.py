@@ -123,6 +123,13 @@ SIGNATURES = {
     "tg_cone_tv_reconstruct_host": (c_int, [c_vp, c_vp, c_vp, c_u64, c_dbl, c_dbl, c_dblp]),
     "tg_planar_tv_reconstruct_host": (c_int, [c_vp, c_vp, c_vp, c_u64, c_dbl, c_dbl, c_dblp]),
     "tg_add_gaussian_noise": (c_int, [c_vp, c_vp, c_u64, c_dbl, c_u64]),
+    "tg_axpby": (c_int, [c_vp, c_vp, c_vp, c_u64, c_dbl, c_dbl, c_vp]),
+    "tg_multiply_weights": (c_int, [c_vp, c_vp, c_vp, c_u64, c_u64, c_vp]),
+    "tg_multiply_weights_grad": (c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_u64, c_u64, c_vp]),
+    "tg_fourier_filter": (c_int, [c_vp, c_vp, c_vp, c_u64, c_u64, c_u64, c_vp]),
+    "tg_fourier_filter_weight_grad": (c_int, [c_vp, c_vp, c_vp, c_u64, c_u64, c_u64, c_vp]),
+    "tg_l2_grad": (c_int, [c_vp, c_vp, c_vp, c_vp, c_u64, c_dbl, c_vp]),
+    "tg_tv_grad": (c_int, [c_vp, c_vp, c_u64, c_u64, c_u64, c_dbl, c_vp, c_vp]),
     "tg_kernel_launch_count": (c_u64, []),
     "tg_set_timing": (None, [c_int]),
     "tg_last_kernel_ms": (c_dbl, []),

@@ -29,7 +29,7 @@ CUDA_HOME = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA_HOME, "bin", "nvcc")
 HOST_CXX = "/usr/bin/g++" if os.path.exists("/usr/bin/g++") else "g++"
 
-CU_SOURCES = ["runtime.cu", "cone.cu", "filter.cu", "planar.cu", "phantom.cu", "iterative.cu"]
+CU_SOURCES = ["runtime.cu", "cone.cu", "filter.cu", "planar.cu", "phantom.cu", "iterative.cu", "graph.cu"]
 CPP_SOURCES = ["host_geometry.cpp"]
 HEADERS = ["tg_internal.h", "device_common.cuh", "cone_kernels.cuh", "filter.cuh", "fft16.cuh"]
 

@@ -8,7 +8,9 @@
 // in fp32 with FP64-derived twiddles; parity tolerance is stated in
 // tests/test_gpu_filter.py.
 #include <cmath>
+#include <map>
 #include <memory>
+#include <mutex>
 #include <vector>
 
 #include "fft16.cuh"
@@ -275,6 +277,81 @@ void apply(const RowFilter& f, const float* d_in, float* d_out, uint64_t n_rows,
   timer.stop();
 }
 
+// ---- graph fourier_filter node with device-resident (trainable) weights ----
+// graph.hpp:152-164 / 312-316 forward, 470-497 gradients.
+//
+// Re(IFFT(k X)) of a real row equals IFFT(k_s X) with the symmetrised
+// weights k_s[f] = (k[f] + k[P-f]) / 2 (the antisymmetric part only feeds the
+// discarded imaginary part), so every call takes the packed two-rows-per-FFT
+// path of K3 whatever the weights are.
+__global__ void symmetrize_kernel(const float* __restrict__ k, float* __restrict__ ks, int P) {
+  for (int f = blockIdx.x * blockDim.x + threadIdx.x; f < P; f += gridDim.x * blockDim.x)
+    ks[f] = float(0.5 * (double(k[f]) + double(k[(P - f) & (P - 1)])));
+}
+
+// d loss / d k_f = sum over rows Re(X_f conj(G_f)) / P (graph.hpp:478-496).
+// One complex FFT per row pairs x (real part) with g (imaginary part):
+// X_f = (Z_f + conj Z_{P-f}) / 2, G_f = (Z_f - conj Z_{P-f}) / (2i).
+// Each CTA walks rows blockIdx.x, +gridDim.x, ... and keeps per-frequency
+// FP64 sums in shared memory; partial[cta][f] are reduced in a fixed order.
+__global__ void __launch_bounds__(kThreads) filter_weight_grad_kernel(
+    const float* __restrict__ x, const float* __restrict__ g, int n, int P, uint64_t n_rows,
+    const float2* __restrict__ tw, double* __restrict__ partial) {
+  extern __shared__ float2 buf[];
+  float2* zx = buf;
+  float2* zy = buf + P;
+  double* acc = reinterpret_cast<double*>(buf + 2 * P);
+  for (int f = threadIdx.x; f < P; f += blockDim.x) acc[f] = 0.0;
+  for (uint64_t r = blockIdx.x; r < n_rows; r += gridDim.x) {
+    const float* xr = x + r * uint64_t(n);
+    const float* gr = g + r * uint64_t(n);
+    for (int j = threadIdx.x; j < P; j += blockDim.x)
+      zx[j] = j < n ? make_float2(xr[j], gr[j]) : make_float2(0.f, 0.f);
+    __syncthreads();
+    const float2* Z = fft_smem(zx, zy, P, tw, false);
+    for (int f = threadIdx.x; f < P; f += blockDim.x) {
+      const float2 a = Z[f];
+      const float2 c = Z[(P - f) & (P - 1)];  // b = conj(c)
+      const double xr_ = 0.5 * (double(a.x) + double(c.x)), xi_ = 0.5 * (double(a.y) - double(c.y));
+      const double dr = double(a.x) - double(c.x), di = double(a.y) + double(c.y);
+      const double gr_ = 0.5 * di, gi_ = -0.5 * dr;  // (a - b) / (2i)
+      acc[f] += xr_ * gr_ + xi_ * gi_;
+    }
+    __syncthreads();  // the next row reuses the buffers
+  }
+  for (int f = threadIdx.x; f < P; f += blockDim.x) partial[uint64_t(blockIdx.x) * P + f] = acc[f];
+}
+
+__global__ void filter_weight_grad_reduce(const double* __restrict__ partial, int parts, int P,
+                                          double inv_p, float* gk) {
+  for (int f = blockIdx.x * blockDim.x + threadIdx.x; f < P; f += gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int c = 0; c < parts; ++c) s += partial[uint64_t(c) * P + f];
+    gk[f] = float(double(gk[f]) + inv_p * s);
+  }
+}
+
+// per-(device, P) twiddle tables, built once and kept for the process
+const RowFilter& tables(int device, uint64_t P) {
+  static std::mutex mu;
+  static std::map<std::pair<int, uint64_t>, RowFilter*> cache;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find({device, P});
+  if (it != cache.end()) return *it->second;
+  std::vector<double> ones(P, 1.0);
+  RowFilter* f = create(P, P, ones.data(), device);
+  cache[{device, P}] = f;
+  return *f;
+}
+
+void check_fourier(uint64_t n, uint64_t P) {
+  // graph.hpp:156-161 in the reference's order
+  check(n >= 1, "fourier_filter input must have at least one axis");
+  check(is_pow2(P), "filter window must be a power of two");
+  check(P >= n, "filter window is smaller than the detector row");
+  check(P <= 8192, "filter window exceeds the device filter's 8192-sample limit");
+}
+
 }  // namespace filt
 }  // namespace tgb
 
@@ -354,6 +431,52 @@ tg_status tg_apply_row_weights(const float* d_in, float* d_out, uint64_t n_views
     filt::apply_row_weights_kernel<<<unsigned(blocks), 256, 0, as_stream(stream)>>>(
         d_in, d_out, total, n_rows, n, d_map);
     TG_LAUNCHED(1);
+  });
+}
+
+/* graph fourier_filter node: rows of n at window P, device weights k[P] */
+tg_status tg_fourier_filter(const float* d_x, const float* d_k, float* d_out, uint64_t n_rows,
+                            uint64_t n, uint64_t P, void* stream) {
+  return guarded([&] {
+    filt::check_fourier(n, P);
+    if (n_rows == 0) return;
+    int dev = 0;
+    TG_CUDA(cudaGetDevice(&dev));
+    const cudaStream_t st = as_stream(stream);
+    filt::RowFilter f = filt::tables(dev, P);
+    f.n = n;
+    f.symmetric = true;
+    float* ks = nullptr;
+    TG_CUDA(cudaMallocAsync(&ks, P * sizeof(float), st));
+    filt::symmetrize_kernel<<<unsigned((P + 255) / 256), 256, 0, st>>>(d_k, ks, int(P));
+    TG_LAUNCHED(1);
+    f.d_w = ks;
+    filt::apply(f, d_x, d_out, n_rows, nullptr, st);
+    TG_CUDA(cudaFreeAsync(ks, st));
+  });
+}
+
+tg_status tg_fourier_filter_weight_grad(const float* d_x, const float* d_g, float* d_gk,
+                                        uint64_t n_rows, uint64_t n, uint64_t P, void* stream) {
+  return guarded([&] {
+    filt::check_fourier(n, P);
+    if (n_rows == 0) return;
+    int dev = 0;
+    TG_CUDA(cudaGetDevice(&dev));
+    const cudaStream_t st = as_stream(stream);
+    const filt::RowFilter& f = filt::tables(dev, P);
+    const int parts = int(std::min<uint64_t>(n_rows, 2 * 148));
+    double* partial = nullptr;
+    TG_CUDA(cudaMallocAsync(&partial, sizeof(double) * P * parts, st));
+    const size_t smem = 2 * P * sizeof(float2) + P * sizeof(double);
+    TG_CUDA(cudaFuncSetAttribute(filt::filter_weight_grad_kernel,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    filt::filter_weight_grad_kernel<<<parts, 256, smem, st>>>(d_x, d_g, int(n), int(P), n_rows,
+                                                              f.d_tw, partial);
+    filt::filter_weight_grad_reduce<<<unsigned((P + 255) / 256), 256, 0, st>>>(
+        partial, parts, int(P), 1.0 / double(P), d_gk);
+    TG_LAUNCHED(2);
+    TG_CUDA(cudaFreeAsync(partial, st));
   });
 }
 

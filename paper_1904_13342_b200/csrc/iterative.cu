@@ -19,6 +19,7 @@
 //    subgradient, the data gradient (the back-projection) and the descent
 //    update fused; x is double-buffered.  HBM-bound: 12 B per voxel
 //    (x, grad in; x' out), neighbour re-reads hit L1/L2.
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <mutex>
@@ -96,6 +97,37 @@ struct OutList {
   int n;
 };
 
+// subgradient count s_i of voxel i and the TV of the forward pairs it owns
+// (graph.hpp:365-377, 511-528; axes x, y, z in the reference's order)
+__device__ __forceinline__ int tv_stencil(const float* __restrict__ x, long long i, int nx, int ny,
+                                          int nz, long long plane, int has_lo, int has_hi,
+                                          double& tv) {
+  const int ix = int(i % nx);
+  const long long r = i / nx;
+  const int iy = int(r % ny), iz = int(r / ny);
+  const double xi = x[i];
+  int s = 0;
+  if (ix >= 1) s += sgn(xi - double(x[i - 1]));
+  if (ix + 1 < nx) {
+    const double d = double(x[i + 1]) - xi;
+    s -= sgn(d);
+    tv += fabs(d);
+  }
+  if (iy >= 1) s += sgn(xi - double(x[i - nx]));
+  if (iy + 1 < ny) {
+    const double d = double(x[i + nx]) - xi;
+    s -= sgn(d);
+    tv += fabs(d);
+  }
+  if (iz >= 1 || has_lo) s += sgn(xi - double(x[i - plane]));
+  if (iz + 1 < nz || has_hi) {
+    const double d = double(x[i + plane]) - xi;
+    s -= sgn(d);
+    tv += fabs(d);
+  }
+  return s;
+}
+
 __global__ void __launch_bounds__(kRedThreads) tv_step_kernel(
     const float* __restrict__ x, const float* __restrict__ grad, const OutList outs, int nx,
     int ny, int nz, int has_lo, int has_hi, double lambda, double lr, double* __restrict__ partial) {
@@ -104,30 +136,9 @@ __global__ void __launch_bounds__(kRedThreads) tv_step_kernel(
   double tv = 0.0;
   const long long stride = (long long)gridDim.x * blockDim.x;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-    const int ix = int(i % nx);
-    const long long r = i / nx;
-    const int iy = int(r % ny), iz = int(r / ny);
-    const double xi = x[i];
-    int s = 0;
-    if (ix >= 1) s += sgn(xi - double(x[i - 1]));
-    if (ix + 1 < nx) {
-      const double d = double(x[i + 1]) - xi;
-      s -= sgn(d);
-      tv += fabs(d);
-    }
-    if (iy >= 1) s += sgn(xi - double(x[i - nx]));
-    if (iy + 1 < ny) {
-      const double d = double(x[i + nx]) - xi;
-      s -= sgn(d);
-      tv += fabs(d);
-    }
-    if (iz >= 1 || has_lo) s += sgn(xi - double(x[i - plane]));
-    if (iz + 1 < nz || has_hi) {
-      const double d = double(x[i + plane]) - xi;
-      s -= sgn(d);
-      tv += fabs(d);
-    }
+    const int s = tv_stencil(x, i, nx, ny, nz, plane, has_lo, has_hi, tv);
     if (outs.n) {
+      const double xi = x[i];
       const double g = lambda * double(s) + double(grad[i]);
       const float v = float(xi - lr * g);
 #pragma unroll 1
@@ -136,6 +147,36 @@ __global__ void __launch_bounds__(kRedThreads) tv_step_kernel(
   }
   tv = block_sum(tv);
   if (threadIdx.x == 0) partial[blockIdx.x] = tv;
+}
+
+// the backward of a graph tv_loss node alone (graph.hpp:511-528, upstream
+// gradient gs): gx_i += gs * s_i, plus the TV value.  gx must not alias x.
+__global__ void __launch_bounds__(kRedThreads) tv_grad_kernel(const float* __restrict__ x,
+                                                              float* __restrict__ gx, int nx,
+                                                              int ny, int nz, double gs,
+                                                              double* __restrict__ partial) {
+  const long long plane = (long long)nx * ny;
+  const long long n = plane * nz;
+  double tv = 0.0;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const int s = tv_stencil(x, i, nx, ny, nz, plane, 0, 0, tv);
+    if (s) gx[i] = float(double(gx[i]) + gs * double(s));
+  }
+  tv = block_sum(tv);
+  if (threadIdx.x == 0) partial[blockIdx.x] = tv;
+}
+
+// the backward of a graph l2_loss node (graph.hpp:498-509, upstream gs):
+// d = 2 gs (a - b); ga += d; gb -= d (either may be null)
+__global__ void l2_grad_kernel(const float* __restrict__ a, const float* __restrict__ b,
+                               float* ga, float* gb, uint64_t n, double gs2) {
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const double d = gs2 * (double(a[i]) - double(b[i]));
+    if (ga) ga[i] = float(double(ga[i]) + d);
+    if (gb) gb[i] = float(double(gb[i]) - d);
+  }
 }
 
 // stream-ordered device buffer (pool-backed: no device-wide sync)
@@ -384,6 +425,32 @@ tg_status tg_tv_step(const float* d_x, const float* d_grad, float* d_x_out, uint
     iter::Scratch sc(st);
     iter::tv_step(d_x, d_grad, iter::one_out(d_x_out), nx, ny, nz, has_lo != 0, has_hi != 0,
                   tv_lambda, learning_rate, d_tv, st, sc);
+  });
+}
+
+tg_status tg_tv_grad(const float* d_x, float* d_gx, uint64_t nx, uint64_t ny, uint64_t nz,
+                     double gs, double* d_tv, void* stream) {
+  return guarded([&] {
+    check(nx >= 1 && ny >= 1 && nz >= 1, "tv_loss needs a non-scalar input");
+    check(d_gx != nullptr && d_gx != d_x, "tv_grad: the gradient must not alias x");
+    const cudaStream_t st = as_stream(stream);
+    iter::Scratch sc(st);
+    iter::tv_grad_kernel<<<iter::kRedBlocks, iter::kRedThreads, 0, st>>>(
+        d_x, d_gx, int(nx), int(ny), int(nz), gs, sc.partial);
+    iter::sum_partials_kernel<<<1, iter::kRedThreads, 0, st>>>(sc.partial, iter::kRedBlocks,
+                                                               d_tv);
+    TG_LAUNCHED(2);
+  });
+}
+
+tg_status tg_l2_grad(const float* d_a, const float* d_b, float* d_ga, float* d_gb, uint64_t n,
+                     double gs, void* stream) {
+  return guarded([&] {
+    if (n == 0 || (!d_ga && !d_gb)) return;
+    const cudaStream_t st = as_stream(stream);
+    const uint64_t blocks = std::min<uint64_t>((n + 255) / 256, 148 * 16);
+    iter::l2_grad_kernel<<<unsigned(blocks), 256, 0, st>>>(d_a, d_b, d_ga, d_gb, n, 2.0 * gs);
+    TG_LAUNCHED(1);
   });
 }
 

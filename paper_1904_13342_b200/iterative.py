@@ -18,6 +18,8 @@ from __future__ import annotations
 from dataclasses import dataclass, field
 from typing import List, Tuple
 
+import math
+
 import numpy as np
 import torch
 
@@ -160,3 +162,86 @@ def experiment_iterative_tv(geo: ParallelGeometry, cfg: ExperimentConfig, device
     r.fbp_reference = fbp_reconstruct(r.noisy_sinogram, geo, FilterKind.ramlak)
     r.reconstruction, r.loss_history = tv_reconstruct(r.noisy_sinogram, geo, cfg)
     return r
+
+
+# ---- reconstruction-filter learning (pipelines.hpp:181-261) ---------------
+
+
+@dataclass
+class FilterLearningResult:
+    """pipelines.hpp:183-190"""
+    loss_history: List[float] = field(default_factory=list)
+    distance_history: List[float] = field(default_factory=list)
+    learned_weights: np.ndarray = None
+    ramp_init: object = None
+    ramlak_reference: object = None
+    reconstruction: Image = None
+
+
+def learn_filter(sino: Sinogram, geo: ParallelGeometry, cfg: ExperimentConfig,
+                 r: FilterLearningResult = None) -> FilterLearningResult:
+    """pipelines.hpp:202-259 on a given sinogram: frequency weights K start at
+    the ramp and descend on |pi/n BP(filter(p, K)) - FBP_ramlak(p)|^2 through the
+    device graph (graph.Graph: K3 filter + K6 back-projection forward, K8 /
+    scale / K7 / filter weight-gradient backward)."""
+    from .filtering import ramlak_filter, ramp_filter
+    from .graph import Graph, gradient_descent_step
+    from .pipelines import fbp_reconstruct
+    check(isinstance(geo, ParallelGeometry), "learn-filter expects a parallel-beam geometry")
+    r = r or FilterLearningResult()
+    r.ramp_init = ramp_filter(geo.detector.n_bins, geo.detector.spacing, cfg.filter_window)
+    r.ramlak_reference = ramlak_filter(geo.detector.n_bins, geo.detector.spacing,
+                                       cfg.filter_window)
+    padded = r.ramp_init.padded_n
+    ramlak_w = r.ramlak_reference.weights
+    gap = float(np.sqrt(np.sum((r.ramp_init.weights - ramlak_w) ** 2)))
+    data = sino.data
+    check(isinstance(data, torch.Tensor) and data.is_cuda,
+          "learn_filter runs on the device: pass a CUDA sinogram")
+    reference = fbp_reconstruct(sino, geo, r.ramlak_reference)
+    g = Graph(device=data.device)
+    p = g.input(sino.shape())
+    K = g.parameter(torch.from_numpy(r.ramp_init.weights.astype(np.float32)), trainable=True)
+    target = g.parameter(reference.data, trainable=False)
+    filtered = g.fourier_filter(p, K, padded)
+    bp = g.backproject(filtered, geo)
+    recon = g.scale(bp, math.pi / float(geo.n_projections))
+    loss = g.l2_loss(recon, target)
+    feeds = {p: data}
+
+    def record():
+        r.loss_history.append(float(g.value(loss)))
+        w = g.node(K).value.double().cpu().numpy()
+        d = float(np.sqrt(np.sum((w - ramlak_w) ** 2)))
+        r.distance_history.append(d / gap if gap > 0.0 else 0.0)
+
+    def converging(it):
+        if not math.isfinite(r.loss_history[-1]):
+            raise N.Error(f"optimization diverged at iteration {it} (loss is not finite); "
+                          "lower the learning rate")
+
+    for it in range(int(cfg.iterations)):
+        g.forward(feeds)
+        record()
+        converging(it)
+        grads = g.backward(loss)
+        gradient_descent_step(g, grads, cfg.learning_rate)
+    g.forward(feeds)
+    record()
+    converging(int(cfg.iterations))
+    r.learned_weights = g.node(K).value.double().cpu().numpy()
+    r.reconstruction = Image(geo.volume, g.value(recon).clone())
+    return r
+
+
+def experiment_learn_filter(geo: ParallelGeometry, cfg: ExperimentConfig,
+                            device=None) -> FilterLearningResult:
+    """pipelines.hpp:196-261: phantom -> forward projection -> optional noise ->
+    filter learning, all on the device."""
+    from .projector import forward_project
+    check(isinstance(geo, ParallelGeometry), "learn-filter expects a parallel-beam geometry")
+    phantom = make_phantom_2d(cfg.phantom, geo.volume, device)
+    sino = forward_project(phantom, geo)
+    if cfg.noise_relative_std > 0.0:
+        sino = add_gaussian_noise(sino, cfg.noise_relative_std, cfg.seed)
+    return learn_filter(sino, geo, cfg)
