@@ -13,9 +13,9 @@ byte-identical run to run (deterministic kernels; acceptance.cpp:486-548).
 
 Differences, by design: ``reconstruct iterative --geometry`` accepts every
 geometry type (the reference's graph nodes do; its CLI restricts to
-parallel2d) so the config-5 cone loop is reachable from the shell;
-``learn-filter`` (training Fourier filter weights through the graph,
-pipelines.hpp:191-261) is not part of the projector path and reports so.
+parallel2d) so the config-5 cone loop is reachable from the shell.
+``learn-filter`` (pipelines.hpp:191-261) trains the Fourier filter weights
+through the device graph (graph.py).
 """
 from __future__ import annotations
 
@@ -137,7 +137,8 @@ def _build() -> argparse.ArgumentParser:
     p.add_argument("--lr", type=float, default=1e-3)
     p.add_argument("--iterations", type=int, default=100)
 
-    p = sub.add_parser("learn-filter", help="(not on the B200 projector path)")
+    p = sub.add_parser("learn-filter",
+                       help="train reconstruction-filter weights against a known phantom")
     p.add_argument("--config", required=True)
 
     p = sub.add_parser("profile", help="extract a line profile as CSV")
@@ -267,9 +268,28 @@ def _run(a) -> None:
         tio.write_image(a.out, rec)
         if a.loss_csv:
             tio.write_csv(a.loss_csv, ["iteration", "loss"], _history_rows(hist))
-    elif a.cmd == "learn-filter":
-        raise Error("learn-filter trains Fourier filter weights through the reference's graph "
-                    "(pipelines.hpp:191-261); it is not part of the B200 projector path")
+    elif a.cmd == "learn-filter":  # cli.hpp:265-288
+        from .iterative import experiment_learn_filter
+        exp = tio.load_experiment_config(a.config)
+        g = _expect(exp.geometry, ParallelGeometry, "learn-filter", "parallel2d")
+        r = experiment_learn_filter(g, exp.cfg, device=_device())
+        for role, path in exp.outputs.items():
+            if role == "filter_csv":
+                tio.write_filter_csv(path, r.learned_weights)
+            elif role == "ramp_csv":
+                tio.write_filter_csv(path, r.ramp_init.weights)
+            elif role == "ramlak_csv":
+                tio.write_filter_csv(path, r.ramlak_reference.weights)
+            elif role == "loss_csv":
+                tio.write_csv(path, ["iteration", "loss"], _history_rows(r.loss_history))
+            elif role == "distance_csv":
+                tio.write_csv(path, ["iteration", "distance"], _history_rows(r.distance_history))
+            elif role == "image":
+                tio.write_image(path, r.reconstruction)
+            elif role == "profile_csv":
+                _central_profile(path, r.reconstruction)
+            else:
+                raise Error(f"unknown output role '{role}'")
     elif a.cmd == "profile":  # cli.hpp:290-313
         img = _slice_for_display(tio.read_image(a.image), a.slice)
         axis = 0 if a.axis == "x" else 1

@@ -170,6 +170,7 @@ class Graph:
 
     def __init__(self, device=None):
         self._nodes: List[Node] = []
+        self._nan_slots = None
         self.device = torch.device(device) if device is not None else None
 
     # --- builders (graph.hpp:104-190) ----------------------------------------
@@ -284,9 +285,24 @@ class Graph:
                 if not active[i]:
                     active[i] = True
                     stack.append(i)
-        for nid in range(loss, -1, -1):
-            if active[nid]:
-                self._propagate(nid)
+        # graph.hpp:402-406 NaN checks: one device reduction per tensor
+        # gradient into its own slot, read back once after the sweep (the
+        # first offending node in sweep order is reported, as the reference)
+        tensors = [i for i in range(loss + 1)
+                   if active[i] and isinstance(self._nodes[i].grad, torch.Tensor)]
+        if tensors:
+            self._nan_slots = torch.zeros(len(self._nodes), dtype=torch.float64,
+                                          device=self._nodes[tensors[0]].grad.device)
+        try:
+            for nid in range(loss, -1, -1):
+                if active[nid]:
+                    self._propagate(nid)
+        finally:
+            slots = self._nan_slots.cpu().numpy() if tensors else None
+            self._nan_slots = None
+        for nid in sorted(tensors, reverse=True):
+            if math.isnan(slots[nid]):
+                raise N.Error(f"gradient of node {nid} contains NaN")
         return {nid: n.grad for nid, n in enumerate(self._nodes) if n.kind == OpKind.parameter}
 
     def value(self, nid: NodeId):
@@ -362,12 +378,16 @@ class Graph:
         raise N.Error("node kind cannot be evaluated")
 
     def _check_grad_finite(self, nid: NodeId) -> None:
-        """graph.hpp:402-406 (a device reduction; non-finite entries count as NaN)"""
+        """graph.hpp:402-406; tensor gradients: sum (g - g)^2 is NaN iff an
+        entry is not finite, reduced on the device into this node's slot"""
         g = self._nodes[nid].grad
-        bad = (math.isnan(g) if not isinstance(g, torch.Tensor)
-               else math.isnan(_l2_value(g, g)))
-        if bad:
-            raise N.Error(f"gradient of node {nid} contains NaN")
+        if not isinstance(g, torch.Tensor):
+            if math.isnan(g):
+                raise N.Error(f"gradient of node {nid} contains NaN")
+            return
+        slot = self._nan_slots.data_ptr() + 8 * nid
+        N.check(N.lib().tg_l2_residual(g.data_ptr(), g.data_ptr(), None, g.numel(), slot,
+                                       stream_of(g)))
 
     def _add_grad(self, nid: NodeId, contrib, factor: float = 1.0) -> None:
         dst = self._nodes[nid]

@@ -115,3 +115,40 @@ def test_config_runs(tmp_path, tg):
     assert cli.run(["reconstruct", "iterative", "--config", tv]) == 0
     h, rows = tio.read_csv(str(tmp_path / "tv" / "loss.csv"))
     assert h == ["iteration", "loss"] and len(rows) == 41 and rows[-1][1] < rows[0][1]
+
+
+GEO_LEARN = {"type": "parallel2d", "volume_shape": [45, 45], "volume_spacing": [1.0, 1.0],
+             "detector_shape": [64], "detector_spacing": [1.0], "n_projections": 60,
+             "angular_range_deg": 180.0}
+
+
+def test_learn_filter_rejects_non_parallel(tmp_path, capsys):
+    _j(tmp_path / "cone.json", GEO_FDK)
+    cfg = _j(tmp_path / "lf.json", {"geometry": "cone.json", "iterations": 1})
+    assert cli.run(["learn-filter", "--config", cfg]) == 2
+    assert "learn-filter expects a parallel2d geometry" in capsys.readouterr().err
+
+
+@pytest.mark.gpu
+def test_learn_filter_config(tmp_path, tg):
+    """configs/learn_filter.json (noise 0.3, lr 1.5e-5, window 64), 60 of its
+    5000 steps: every output role written, the loss and the distance to
+    Ram-Lak fall, and the run is byte-identical when repeated"""
+    _j(tmp_path / "lfg.json", GEO_LEARN)
+    outs = {"filter_csv": "o/learned.csv", "ramp_csv": "o/ramp.csv", "ramlak_csv": "o/ramlak.csv",
+            "loss_csv": "o/loss.csv", "distance_csv": "o/dist.csv", "image": "o/rec.json",
+            "profile_csv": "o/prof.csv"}
+    cfg = _j(tmp_path / "lf.json", {
+        "geometry": "lfg.json", "phantom": "shepp-logan", "noise_relative_std": 0.3,
+        "learning_rate": 1.5e-5, "iterations": 60, "seed": 1337, "filter_window": 64,
+        "outputs": outs})
+    assert cli.run(["learn-filter", "--config", cfg]) == 0
+    h, rows = tio.read_csv(str(tmp_path / "o" / "loss.csv"))
+    assert h == ["iteration", "loss"] and len(rows) == 61 and rows[-1][1] < rows[0][1]
+    h, rows = tio.read_csv(str(tmp_path / "o" / "dist.csv"))
+    assert h == ["iteration", "distance"] and rows[0][1] == 1.0 and rows[-1][1] < 1.0
+    assert len(tio.read_filter_csv(str(tmp_path / "o" / "learned.csv"))) == 64
+    first = {k: (tmp_path / v).read_bytes() for k, v in outs.items() if not v.endswith(".json")}
+    assert cli.run(["learn-filter", "--config", cfg]) == 0
+    assert first == {k: (tmp_path / v).read_bytes() for k, v in outs.items()
+                     if not v.endswith(".json")}
