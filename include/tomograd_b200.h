@@ -329,6 +329,18 @@ tg_status tg_l2_grad(const float* d_a, const float* d_b, float* d_ga, float* d_g
 tg_status tg_tv_grad(const float* d_x, float* d_gx, uint64_t nx, uint64_t ny, uint64_t nz,
                      double gs, double* d_tv, void* stream);
 
+/* pipelines.hpp:202-259 (experiment_learn_filter's loop), device resident on
+ * a parallel / fan plan: frequency weights K (d_k: P floats; in: the initial
+ * weights, out: the learned ones) descend on |pi/n BP(fourier_filter(p, K)) -
+ * target|^2 at learning_rate.  h_init / h_ramlak (P doubles, host): the initial
+ * and Ram-Lak weights for the recorded distance |K - ramlak| / |init - ramlak|.
+ * h_loss / h_dist: iterations + 1 entries (NULL allowed); d_recon (NULL
+ * allowed): the final reconstruction.  Non-finite loss -> TG_ERROR with the
+ * reference's message. */
+tg_status tg_planar_learn_filter(tg_planar_plan* plan, const float* d_sino, const float* d_target,
+                                 float* d_k, uint64_t P, const double* h_init,
+                                 const double* h_ramlak, double learning_rate, uint64_t iterations,
+                                 double* h_loss, double* h_dist, float* d_recon, void* stream);
 /* pipelines.hpp:119-132 add_gaussian_noise (host, bit-exact: std::mt19937_64
  * Box-Muller of pipelines.hpp:90-115; sigma = relative_std * max(in)) */
 tg_status tg_add_gaussian_noise(const float* h_in, float* h_out, uint64_t n, double relative_std,

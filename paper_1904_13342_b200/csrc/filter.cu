@@ -323,11 +323,11 @@ __global__ void __launch_bounds__(kThreads) filter_weight_grad_kernel(
 }
 
 __global__ void filter_weight_grad_reduce(const double* __restrict__ partial, int parts, int P,
-                                          double inv_p, float* gk) {
+                                          double inv_p, float* gk, int accumulate) {
   for (int f = blockIdx.x * blockDim.x + threadIdx.x; f < P; f += gridDim.x * blockDim.x) {
     double s = 0.0;
     for (int c = 0; c < parts; ++c) s += partial[uint64_t(c) * P + f];
-    gk[f] = float(double(gk[f]) + inv_p * s);
+    gk[f] = accumulate ? float(double(gk[f]) + inv_p * s) : float(inv_p * s);
   }
 }
 
@@ -350,6 +350,41 @@ void check_fourier(uint64_t n, uint64_t P) {
   check(is_pow2(P), "filter window must be a power of two");
   check(P >= n, "filter window is smaller than the detector row");
   check(P <= 8192, "filter window exceeds the device filter's 8192-sample limit");
+}
+
+void fourier_filter(const float* d_x, const float* d_k, float* d_ks, float* d_out,
+                    uint64_t n_rows, uint64_t n, uint64_t P, cudaStream_t st) {
+  check_fourier(n, P);
+  if (n_rows == 0) return;
+  int dev = 0;
+  TG_CUDA(cudaGetDevice(&dev));
+  RowFilter f = tables(dev, P);
+  f.n = n;
+  f.symmetric = true;
+  symmetrize_kernel<<<unsigned((P + 255) / 256), 256, 0, st>>>(d_k, d_ks, int(P));
+  TG_LAUNCHED(1);
+  f.d_w = d_ks;
+  apply(f, d_x, d_out, n_rows, nullptr, st);
+}
+
+int weight_grad_parts(uint64_t n_rows) { return int(std::min<uint64_t>(n_rows, 2 * 148)); }
+
+void weight_grad(const float* d_x, const float* d_g, float* d_gk, double* d_partial,
+                 uint64_t n_rows, uint64_t n, uint64_t P, bool accumulate, cudaStream_t st) {
+  check_fourier(n, P);
+  if (n_rows == 0) return;
+  int dev = 0;
+  TG_CUDA(cudaGetDevice(&dev));
+  const RowFilter& f = tables(dev, P);
+  const int parts = weight_grad_parts(n_rows);
+  const size_t smem = 2 * P * sizeof(float2) + P * sizeof(double);
+  TG_CUDA(cudaFuncSetAttribute(filter_weight_grad_kernel,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  filter_weight_grad_kernel<<<parts, 256, smem, st>>>(d_x, d_g, int(n), int(P), n_rows, f.d_tw,
+                                                      d_partial);
+  filter_weight_grad_reduce<<<unsigned((P + 255) / 256), 256, 0, st>>>(
+      d_partial, parts, int(P), 1.0 / double(P), d_gk, int(accumulate));
+  TG_LAUNCHED(2);
 }
 
 }  // namespace filt
@@ -440,18 +475,10 @@ tg_status tg_fourier_filter(const float* d_x, const float* d_k, float* d_out, ui
   return guarded([&] {
     filt::check_fourier(n, P);
     if (n_rows == 0) return;
-    int dev = 0;
-    TG_CUDA(cudaGetDevice(&dev));
     const cudaStream_t st = as_stream(stream);
-    filt::RowFilter f = filt::tables(dev, P);
-    f.n = n;
-    f.symmetric = true;
     float* ks = nullptr;
     TG_CUDA(cudaMallocAsync(&ks, P * sizeof(float), st));
-    filt::symmetrize_kernel<<<unsigned((P + 255) / 256), 256, 0, st>>>(d_k, ks, int(P));
-    TG_LAUNCHED(1);
-    f.d_w = ks;
-    filt::apply(f, d_x, d_out, n_rows, nullptr, st);
+    filt::fourier_filter(d_x, d_k, ks, d_out, n_rows, n, P, st);
     TG_CUDA(cudaFreeAsync(ks, st));
   });
 }
@@ -461,21 +488,10 @@ tg_status tg_fourier_filter_weight_grad(const float* d_x, const float* d_g, floa
   return guarded([&] {
     filt::check_fourier(n, P);
     if (n_rows == 0) return;
-    int dev = 0;
-    TG_CUDA(cudaGetDevice(&dev));
     const cudaStream_t st = as_stream(stream);
-    const filt::RowFilter& f = filt::tables(dev, P);
-    const int parts = int(std::min<uint64_t>(n_rows, 2 * 148));
     double* partial = nullptr;
-    TG_CUDA(cudaMallocAsync(&partial, sizeof(double) * P * parts, st));
-    const size_t smem = 2 * P * sizeof(float2) + P * sizeof(double);
-    TG_CUDA(cudaFuncSetAttribute(filt::filter_weight_grad_kernel,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    filt::filter_weight_grad_kernel<<<parts, 256, smem, st>>>(d_x, d_g, int(n), int(P), n_rows,
-                                                              f.d_tw, partial);
-    filt::filter_weight_grad_reduce<<<unsigned((P + 255) / 256), 256, 0, st>>>(
-        partial, parts, int(P), 1.0 / double(P), d_gk);
-    TG_LAUNCHED(2);
+    TG_CUDA(cudaMallocAsync(&partial, sizeof(double) * P * filt::weight_grad_parts(n_rows), st));
+    filt::weight_grad(d_x, d_g, d_gk, partial, n_rows, n, P, true, st);
     TG_CUDA(cudaFreeAsync(partial, st));
   });
 }

@@ -31,6 +31,15 @@ struct PreWeights {
 };
 
 RowFilter* create(uint64_t n, uint64_t P, const double* weights, int device);
+
+// graph fourier_filter node (device weights k[P], any real values; d_ks: P
+// floats of scratch for the symmetrised copy) and its weight gradient
+// gk (+)= sum_rows Re(X conj G) / P (d_partial: weight_grad_parts(n_rows) * P doubles)
+void fourier_filter(const float* d_x, const float* d_k, float* d_ks, float* d_out,
+                    uint64_t n_rows, uint64_t n, uint64_t P, cudaStream_t st);
+int weight_grad_parts(uint64_t n_rows);
+void weight_grad(const float* d_x, const float* d_g, float* d_gk, double* d_partial,
+                 uint64_t n_rows, uint64_t n, uint64_t P, bool accumulate, cudaStream_t st);
 void destroy(RowFilter* f);
 void apply(const RowFilter& f, const float* d_in, float* d_out, uint64_t n_rows,
            const PreWeights* pw, cudaStream_t st);

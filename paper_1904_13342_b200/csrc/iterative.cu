@@ -27,6 +27,7 @@
 #include <vector>
 
 #include "device_common.cuh"
+#include "filter.cuh"
 
 namespace tgb {
 namespace iter {
@@ -371,6 +372,126 @@ void tv_loop(Fwd fwd, Bwd bwd, uint64_t n_sino, uint64_t nx, uint64_t ny, uint64
   }
 }
 
+// ---- filter learning (pipelines.hpp:202-259), device resident ------------
+// One step on the trainable weights K (in place):
+//   filtered = fourier_filter(p, K)             K3 (graph.hpp:312-316)
+//   recon    = (pi / n) BP(filtered)            K6, scale node fused in the epilogue
+//   loss     = |recon - target|^2, g = 2 (pi/n) (recon - target)   K8 (l2 + scale gradients)
+//   gfil     = FP(g)                            K7 (backproject's registered gradient)
+//   gK       = sum_rows Re(P conj G) / P        filter weight gradient (graph.hpp:478-496)
+//   K       -= lr gK                            graph.hpp:533-546
+// The recorded distance |K - ramlak|^2 is reduced on the device too, so a
+// captured step needs no host round trip; one step is captured into a CUDA
+// graph and replayed.
+__global__ void lf_record_kernel(const double* __restrict__ loss_slot, const float* __restrict__ K,
+                                 const double* __restrict__ ramlak, int P,
+                                 double* __restrict__ hist, int* __restrict__ counter) {
+  double d2 = 0.0;
+  for (int k = threadIdx.x; k < P; k += blockDim.x) {
+    const double d = double(K[k]) - ramlak[k];
+    d2 += d * d;
+  }
+  d2 = block_sum(d2);
+  if (threadIdx.x == 0) {
+    const int c = counter[0];
+    hist[2 * c] = loss_slot[0];
+    hist[2 * c + 1] = d2;
+    counter[0] = c + 1;
+  }
+}
+
+__global__ void lf_descent_kernel(float* __restrict__ K, const float* __restrict__ gK, int P,
+                                  double lr) {
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < P; k += gridDim.x * blockDim.x)
+    K[k] = float(double(K[k]) - lr * double(gK[k]));
+}
+
+template <typename Fwd, typename Bwd>
+void learn_filter_loop(Fwd fwd, Bwd bwd, uint64_t n_rows, uint64_t n, uint64_t n_vox,
+                       const float* d_sino, const float* d_target, float* d_k, uint64_t P,
+                       const double* h_init, const double* h_ramlak, double lr,
+                       uint64_t iterations, double factor, double* h_loss, double* h_dist,
+                       float* d_recon, cudaStream_t st) {
+  keep_pool(st);
+  const uint64_t n_sino = n_rows * n;
+  AsyncBuf<float> fil_b(n_sino, st), rec_b(n_vox, st), grec_b(n_vox, st), gfil_b(n_sino, st);
+  AsyncBuf<float> ks_b(P, st), gk_b(P, st);
+  AsyncBuf<double> part_b(size_t(filt::weight_grad_parts(n_rows)) * P, st);
+  AsyncBuf<double> ramlak_b(P, st), hist_b(2 * (iterations + 1), st), slot_b(1, st);
+  AsyncBuf<int> ctr_b(1, st);
+  TG_CUDA(cudaMemcpyAsync(ramlak_b.p, h_ramlak, P * sizeof(double), cudaMemcpyHostToDevice, st));
+  TG_CUDA(cudaMemsetAsync(ctr_b.p, 0, sizeof(int), st));
+  Scratch sc(st);
+  auto forward = [&](cudaStream_t s, bool with_grad) {
+    filt::fourier_filter(d_sino, d_k, ks_b.p, fil_b.p, n_rows, n, P, s);
+    bwd(fil_b.p, rec_b.p, float(factor), s);
+    l2_residual_kernel<<<kRedBlocks, kRedThreads, 0, s>>>(
+        rec_b.p, d_target, with_grad ? grec_b.p : nullptr, n_vox, 2.0 * factor, sc.partial);
+    sum_partials_kernel<<<1, kRedThreads, 0, s>>>(sc.partial, kRedBlocks, slot_b.p);
+    lf_record_kernel<<<1, kRedThreads, 0, s>>>(slot_b.p, d_k, ramlak_b.p, int(P), hist_b.p,
+                                               ctr_b.p);
+    TG_LAUNCHED(3);
+  };
+  auto step = [&](cudaStream_t s) {
+    forward(s, true);
+    fwd(grec_b.p, gfil_b.p, s);
+    filt::weight_grad(d_sino, gfil_b.p, gk_b.p, part_b.p, n_rows, n, P, false, s);
+    lf_descent_kernel<<<unsigned((P + 255) / 256), 256, 0, s>>>(d_k, gk_b.p, int(P), lr);
+    TG_LAUNCHED(1);
+  };
+  uint64_t it = 0;
+  if (iterations >= 4) {
+    step(st);  // un-captured: plan state and kernel attributes settle
+    ++it;
+    cudaStream_t gs;
+    cudaEvent_t ev;
+    TG_CUDA(cudaStreamCreateWithFlags(&gs, cudaStreamNonBlocking));
+    TG_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    TG_CUDA(cudaEventRecord(ev, st));
+    TG_CUDA(cudaStreamWaitEvent(gs, ev, 0));
+    const uint64_t launches0 = tg_kernel_launch_count();
+    TG_CUDA(cudaStreamBeginCapture(gs, cudaStreamCaptureModeThreadLocal));
+    step(gs);
+    cudaGraph_t g;
+    TG_CUDA(cudaStreamEndCapture(gs, &g));
+    const uint64_t per_replay = tg_kernel_launch_count() - launches0;
+    cudaGraphExec_t ge;
+    TG_CUDA(cudaGraphInstantiate(&ge, g, 0));
+    const uint64_t replays = iterations - it;
+    for (uint64_t r = 0; r < replays; ++r) TG_CUDA(cudaGraphLaunch(ge, gs));
+    count_launch(per_replay * (replays ? replays - 1 : 0));
+    it += replays;
+    TG_CUDA(cudaEventRecord(ev, gs));
+    TG_CUDA(cudaStreamWaitEvent(st, ev, 0));
+    TG_CUDA(cudaStreamSynchronize(gs));
+    cudaGraphExecDestroy(ge);
+    cudaGraphDestroy(g);
+    cudaEventDestroy(ev);
+    cudaStreamDestroy(gs);
+  }
+  for (; it < iterations; ++it) step(st);
+  forward(st, false);
+  if (d_recon)
+    TG_CUDA(cudaMemcpyAsync(d_recon, rec_b.p, n_vox * sizeof(float), cudaMemcpyDeviceToDevice, st));
+  std::vector<double> h(2 * (iterations + 1));
+  TG_CUDA(cudaMemcpyAsync(h.data(), hist_b.p, h.size() * sizeof(double), cudaMemcpyDeviceToHost,
+                          st));
+  TG_CUDA(cudaStreamSynchronize(st));
+  double gap = 0.0;
+  for (uint64_t k = 0; k < P; ++k) {
+    const double d = h_init[k] - h_ramlak[k];
+    gap += d * d;
+  }
+  gap = std::sqrt(gap);
+  for (uint64_t i = 0; i <= iterations; ++i) {
+    if (h_loss) h_loss[i] = h[2 * i];
+    if (h_dist) h_dist[i] = gap > 0.0 ? std::sqrt(h[2 * i + 1]) / gap : 0.0;
+    if (!std::isfinite(h[2 * i]))
+      throw RefError("optimization diverged at iteration " + std::to_string(i) +
+                     " (loss is not finite); lower the learning rate");
+  }
+}
+
 // host-buffer forms of the loop: one upload, the device loop, one download
 template <typename Run>
 tg_status tv_host(int device, uint64_t n_sino, uint64_t n_vox, const float* h_sino, float* h_x,
@@ -589,6 +710,32 @@ tg_status tg_cone_tv_reconstruct(tg_cone_plan* plan, const float* d_sino, float*
         },
                   n_proj * det.n_u * det.n_v, vol.shape[0], vol.shape[1], vol.shape[2], d_sino,
                   d_x, iterations, learning_rate, tv_lambda, h_loss_history, st);
+  });
+}
+
+tg_status tg_planar_learn_filter(tg_planar_plan* plan, const float* d_sino, const float* d_target,
+                                 float* d_k, uint64_t P, const double* h_init,
+                                 const double* h_ramlak, double learning_rate, uint64_t iterations,
+                                 double* h_loss, double* h_dist, float* d_recon, void* stream) {
+  return guarded([&] {
+    const cudaStream_t st = as_stream(stream);
+    tg_volume_spec vol;
+    tg_detector1d det;
+    uint64_t n_proj = 0;
+    tg_planar_plan_shape(plan, &vol, &det, &n_proj);
+    check(n_proj <= 2048, "learn_filter: at most 2048 views (one constant-bank view table)");
+    auto ok = [](tg_status s) {
+      if (s != TG_OK) throw RefError(tg_last_error());
+    };
+    // graph: scale(backproject(.), pi / n_projections) (pipelines.hpp:228-229)
+    const double factor = kPi / double(n_proj);
+    iter::learn_filter_loop(
+        [&](const float* x, float* s, cudaStream_t q) { ok(tg_planar_forward(plan, x, s, q)); },
+        [&](const float* s, float* x, float scale, cudaStream_t q) {
+          ok(tg_planar_backproject(plan, s, x, scale, 0, q));
+        },
+        n_proj, det.n_bins, vol.shape[0] * vol.shape[1], d_sino, d_target, d_k, P, h_init,
+        h_ramlak, learning_rate, iterations, factor, h_loss, h_dist, d_recon, st);
   });
 }
 

@@ -179,30 +179,55 @@ class FilterLearningResult:
 
 
 def learn_filter(sino: Sinogram, geo: ParallelGeometry, cfg: ExperimentConfig,
-                 r: FilterLearningResult = None) -> FilterLearningResult:
+                 via_graph: bool = False) -> FilterLearningResult:
     """pipelines.hpp:202-259 on a given sinogram: frequency weights K start at
-    the ramp and descend on |pi/n BP(filter(p, K)) - FBP_ramlak(p)|^2 through the
-    device graph (graph.Graph: K3 filter + K6 back-projection forward, K8 /
-    scale / K7 / filter weight-gradient backward)."""
+    the ramp and descend on |pi/n BP(filter(p, K)) - FBP_ramlak(p)|^2.
+
+    Default: the device-resident loop (tg_planar_learn_filter — K3 filter, K6
+    back-projection, K8, K7, weight gradient and descent per step, one step
+    captured in a CUDA graph and replayed).  ``via_graph``: the same loop
+    built node by node on graph.Graph, exactly as the reference builds it."""
     from .filtering import ramlak_filter, ramp_filter
-    from .graph import Graph, gradient_descent_step
     from .pipelines import fbp_reconstruct
     check(isinstance(geo, ParallelGeometry), "learn-filter expects a parallel-beam geometry")
-    r = r or FilterLearningResult()
+    r = FilterLearningResult()
     r.ramp_init = ramp_filter(geo.detector.n_bins, geo.detector.spacing, cfg.filter_window)
     r.ramlak_reference = ramlak_filter(geo.detector.n_bins, geo.detector.spacing,
                                        cfg.filter_window)
     padded = r.ramp_init.padded_n
-    ramlak_w = r.ramlak_reference.weights
-    gap = float(np.sqrt(np.sum((r.ramp_init.weights - ramlak_w) ** 2)))
     data = sino.data
     check(isinstance(data, torch.Tensor) and data.is_cuda,
           "learn_filter runs on the device: pass a CUDA sinogram")
+    data = data.contiguous()
     reference = fbp_reconstruct(sino, geo, r.ramlak_reference)
+    if via_graph:
+        return _learn_filter_graph(r, data, reference.data, geo, cfg)
+    k = torch.from_numpy(r.ramp_init.weights.astype(np.float32)).to(data.device)
+    it = int(cfg.iterations)
+    loss = np.zeros(it + 1)
+    dist = np.zeros(it + 1)
+    recon = torch.empty_like(reference.data)
+    N.check(N.lib().tg_planar_learn_filter(
+        geo._plan(_dev(data)), data.data_ptr(), reference.data.data_ptr(), k.data_ptr(), padded,
+        N.dptr(r.ramp_init.weights), N.dptr(r.ramlak_reference.weights),
+        float(cfg.learning_rate), it, N.dptr(loss), N.dptr(dist), recon.data_ptr(),
+        stream_of(data)))
+    r.loss_history = [float(v) for v in loss]
+    r.distance_history = [float(v) for v in dist]
+    r.learned_weights = k.double().cpu().numpy()
+    r.reconstruction = Image(geo.volume, recon)
+    return r
+
+
+def _learn_filter_graph(r, data, target_data, geo, cfg) -> FilterLearningResult:
+    from .graph import Graph, gradient_descent_step
+    padded = r.ramp_init.padded_n
+    ramlak_w = r.ramlak_reference.weights
+    gap = float(np.sqrt(np.sum((r.ramp_init.weights - ramlak_w) ** 2)))
     g = Graph(device=data.device)
-    p = g.input(sino.shape())
+    p = g.input(list(reversed(data.shape)))
     K = g.parameter(torch.from_numpy(r.ramp_init.weights.astype(np.float32)), trainable=True)
-    target = g.parameter(reference.data, trainable=False)
+    target = g.parameter(target_data, trainable=False)
     filtered = g.fourier_filter(p, K, padded)
     bp = g.backproject(filtered, geo)
     recon = g.scale(bp, math.pi / float(geo.n_projections))

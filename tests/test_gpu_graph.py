@@ -111,11 +111,13 @@ def _learn_setup(tg):
     return geo, og, sino
 
 
-def test_learn_filter_vs_reference_graph(tg):
-    """configs/learn_filter.json geometry and rate, 40 steps, noise-free"""
+@pytest.mark.parametrize("via_graph", [False, True])
+def test_learn_filter_vs_reference_graph(tg, via_graph):
+    """configs/learn_filter.json geometry and rate, 40 steps, noise-free; the
+    device-resident loop and the node-by-node device graph"""
     geo, og, sino = _learn_setup(tg)
     cfg = tg.ExperimentConfig(learning_rate=1.5e-5, iterations=40, filter_window=64)
-    r = tg.learn_filter(sino, geo, cfg)
+    r = tg.learn_filter(sino, geo, cfg, via_graph=via_graph)
     s64 = sino.data.cpu().numpy().astype(np.float64)
     l_ref, d_ref, w_ref, rec_ref = O.Ref.learn_filter_graph(og, s64, 64, 1.5e-5, 40)
     l_or, d_or, w_or, _ = O.learn_filter_planar(og, s64, 64, 1.5e-5, 40)
@@ -130,6 +132,21 @@ def test_learn_filter_vs_reference_graph(tg):
     assert len(r.loss_history) == 41 and r.loss_history[-1] < r.loss_history[0]
     assert r.distance_history[-1] < r.distance_history[0]
     assert_close(r.reconstruction.data.cpu().numpy(), rec_ref, 1e-4, 1e-3, "learned FBP")
+
+
+def test_learn_filter_loop_matches_graph(tg):
+    """the fused device loop and the node-by-node graph run the same maths"""
+    geo, og, sino = _learn_setup(tg)
+    cfg = tg.ExperimentConfig(learning_rate=1.5e-5, iterations=12, filter_window=64)
+    a = tg.learn_filter(sino, geo, cfg)
+    b = tg.learn_filter(sino, geo, cfg, via_graph=True)
+    np.testing.assert_allclose(a.loss_history, b.loss_history, rtol=2e-6)
+    np.testing.assert_allclose(a.learned_weights, b.learned_weights, rtol=1e-6,
+                               atol=1e-7 * np.abs(b.learned_weights).max())
+    # run-to-run determinism of the captured loop
+    c = tg.learn_filter(sino, geo, cfg)
+    assert a.loss_history == c.loss_history
+    assert np.array_equal(a.learned_weights, c.learned_weights)
 
 
 def test_experiment_learn_filter_end_to_end(tg):
