@@ -341,6 +341,13 @@ tg_status tg_planar_learn_filter(tg_planar_plan* plan, const float* d_sino, cons
                                  float* d_k, uint64_t P, const double* h_init,
                                  const double* h_ramlak, double learning_rate, uint64_t iterations,
                                  double* h_loss, double* h_dist, float* d_recon, void* stream);
+/* the same with host buffers (h_k: initial weights in, learned weights out;
+ * h_recon may be NULL) */
+tg_status tg_planar_learn_filter_host(tg_planar_plan* plan, const float* h_sino,
+                                      const float* h_target, float* h_k, uint64_t P,
+                                      const double* h_init, const double* h_ramlak,
+                                      double learning_rate, uint64_t iterations, double* h_loss,
+                                      double* h_dist, float* h_recon);
 /* pipelines.hpp:119-132 add_gaussian_noise (host, bit-exact: std::mt19937_64
  * Box-Muller of pipelines.hpp:90-115; sigma = relative_std * max(in)) */
 tg_status tg_add_gaussian_noise(const float* h_in, float* h_out, uint64_t n, double relative_std,

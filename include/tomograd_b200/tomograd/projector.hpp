@@ -329,5 +329,43 @@ std::pair<Image<T>, std::vector<double>> tv_reconstruct(const Sinogram<T>& sino,
   return {std::move(img), std::move(hist)};
 }
 
+// pipelines.hpp:211-259 (experiment_learn_filter's graph loop) device
+// resident: frequency weights K start at init_weights (the ramp) and descend
+// on |pi/n BP(fourier_filter(p, K)) - target|^2 (target: the Ram-Lak FBP of p);
+// every step's filter, projections, gradients and update stay in HBM, one
+// step captured as a CUDA graph.  Returns the learned weights, the loss and
+// distance (|K - ramlak| / |init - ramlak|) histories and the reconstruction.
+template <typename T>
+struct LearnFilterResult {
+  std::vector<double> loss_history, distance_history, learned_weights;
+  Image<T> reconstruction;
+};
+
+template <typename T>
+LearnFilterResult<T> learn_filter(const Sinogram<T>& sino, const ParallelGeometry& geo,
+                                  const Image<T>& target, const std::vector<double>& init_weights,
+                                  const std::vector<double>& ramlak_weights, double learning_rate,
+                                  std::size_t iterations) {
+  check(!sino.is_cone() && sino.n_projections == geo.n_projections &&
+            sino.detector1d.n_bins == geo.detector.n_bins,
+        "sinogram shape does not match the geometry");
+  check(init_weights.size() == ramlak_weights.size(),
+        "filter window is inconsistent with its weight vector");
+  LearnFilterResult<T> r;
+  r.reconstruction = Image<T>(geo.volume);
+  F32In<T> in(sino.data), tgt(target.data);
+  std::vector<float> k(init_weights.begin(), init_weights.end());
+  std::vector<float> rec(r.reconstruction.data.size());
+  r.loss_history.resize(iterations + 1);
+  r.distance_history.resize(iterations + 1);
+  throw_if(tg_planar_learn_filter_host(planar_plan(geo, 0.0, 0.0).get(), in.p, tgt.p, k.data(),
+                                       k.size(), init_weights.data(), ramlak_weights.data(),
+                                       learning_rate, iterations, r.loss_history.data(),
+                                       r.distance_history.data(), rec.data()));
+  r.learned_weights.assign(k.begin(), k.end());
+  for (std::size_t i = 0; i < rec.size(); ++i) r.reconstruction.data[i] = T(rec[i]);
+  return r;
+}
+
 }  // namespace b200
 }  // namespace tomograd

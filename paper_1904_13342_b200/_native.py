@@ -132,6 +132,8 @@ SIGNATURES = {
     "tg_tv_grad": (c_int, [c_vp, c_vp, c_u64, c_u64, c_u64, c_dbl, c_vp, c_vp]),
     "tg_planar_learn_filter": (c_int, [c_vp, c_vp, c_vp, c_vp, c_u64, c_dblp, c_dblp, c_dbl, c_u64,
                                        c_dblp, c_dblp, c_vp, c_vp]),
+    "tg_planar_learn_filter_host": (c_int, [c_vp, c_vp, c_vp, c_vp, c_u64, c_dblp, c_dblp, c_dbl,
+                                            c_u64, c_dblp, c_dblp, c_vp]),
     "tg_kernel_launch_count": (c_u64, []),
     "tg_set_timing": (None, [c_int]),
     "tg_last_kernel_ms": (c_dbl, []),

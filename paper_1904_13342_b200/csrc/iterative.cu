@@ -739,6 +739,43 @@ tg_status tg_planar_learn_filter(tg_planar_plan* plan, const float* d_sino, cons
   });
 }
 
+tg_status tg_planar_learn_filter_host(tg_planar_plan* plan, const float* h_sino,
+                                      const float* h_target, float* h_k, uint64_t P,
+                                      const double* h_init, const double* h_ramlak,
+                                      double learning_rate, uint64_t iterations, double* h_loss,
+                                      double* h_dist, float* h_recon) {
+  return guarded([&] {
+    tg_volume_spec vol;
+    tg_detector1d det;
+    uint64_t n_proj = 0;
+    if (tg_planar_plan_shape(plan, &vol, &det, &n_proj) != TG_OK) throw RefError(tg_last_error());
+    const uint64_t n_sino = n_proj * det.n_bins, n_vox = vol.shape[0] * vol.shape[1];
+    cudaStream_t st;
+    TG_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    tg_status r = TG_OK;
+    std::string msg;
+    {
+      iter::AsyncBuf<float> s(n_sino, st), t(n_vox, st), k(P, st), rec(n_vox, st);
+      TG_CUDA(cudaMemcpyAsync(s.p, h_sino, n_sino * sizeof(float), cudaMemcpyHostToDevice, st));
+      TG_CUDA(cudaMemcpyAsync(t.p, h_target, n_vox * sizeof(float), cudaMemcpyHostToDevice, st));
+      TG_CUDA(cudaMemcpyAsync(k.p, h_k, P * sizeof(float), cudaMemcpyHostToDevice, st));
+      r = tg_planar_learn_filter(plan, s.p, t.p, k.p, P, h_init, h_ramlak, learning_rate,
+                                 iterations, h_loss, h_dist, h_recon ? rec.p : nullptr, st);
+      if (r == TG_OK) {
+        TG_CUDA(cudaMemcpyAsync(h_k, k.p, P * sizeof(float), cudaMemcpyDeviceToHost, st));
+        if (h_recon)
+          TG_CUDA(cudaMemcpyAsync(h_recon, rec.p, n_vox * sizeof(float), cudaMemcpyDeviceToHost,
+                                  st));
+      } else {
+        msg = tg_last_error();
+      }
+    }
+    TG_CUDA(cudaStreamSynchronize(st));
+    cudaStreamDestroy(st);
+    if (r != TG_OK) throw RefError(msg);
+  });
+}
+
 tg_status tg_planar_tv_reconstruct(tg_planar_plan* plan, const float* d_sino, float* d_x,
                                    uint64_t iterations, double learning_rate, double tv_lambda,
                                    double* h_loss_history, void* stream) {

@@ -186,6 +186,39 @@ int main() {
     close("b200::tv_reconstruct image vs FP64 loop", rel_err(img2.data, xo), 1e-2, 5e-2);
   }
 
+  // experiment_learn_filter's loop on the device (b200::learn_filter) against
+  // the oracle's FP64 restatement (bitwise the reference's graph,
+  // tests/test_oracle_graph.py) on the reference's learn_filter config
+  {
+    auto v4 = VolumeSpec::centered({45, 45}, {1.0, 1.0});
+    auto g4 = make_parallel(v4, Detector1D::centered(64, 1.0), 60, pi);
+    auto s4 = forward_project(shepp_logan_2d<double>(v4), g4);
+    const Filter1D ramp = ramp_filter(64, 1.0, 64), ramlak = ramlak_filter(64, 1.0, 64);
+    const Image<> target = fbp_reconstruct(s4, g4, ramlak);
+    const std::size_t iters = 30;
+    auto r = b200::learn_filter(s4, g4, target, ramp.weights, ramlak.weights, 1.5e-5, iters);
+    std::vector<double> rays;
+    for (const auto& ray : g4.rays) rays.insert(rays.end(), {ray.x, ray.y});
+    or_planar op{ov(v4), {g4.detector.n_bins, g4.detector.spacing, g4.detector.origin},
+                 g4.n_projections, g4.angular_range, 0.0, 0.0, rays.data(), g4.angles.data()};
+    std::vector<double> lo(iters + 1), dlo(iters + 1), wo(64), reco(45 * 45);
+    or_learn_filter_planar_f64(&op, s4.data.data(), 64, 1.5e-5, iters, lo.data(), dlo.data(),
+                               wo.data(), reco.data());
+    double lmax = 0, wmax = 0, wref = 0;
+    for (std::size_t i = 0; i <= iters; ++i)
+      lmax = std::max(lmax, std::abs(r.loss_history[i] - lo[i]) / lo[i]);
+    for (std::size_t k = 0; k < 64; ++k) {
+      wmax = std::max(wmax, std::abs(r.learned_weights[k] - wo[k]));
+      wref = std::max(wref, std::abs(wo[k]));
+    }
+    report("b200::learn_filter loss history vs FP64 loop", lmax <= 1e-3 && lo.back() < lo.front(),
+           "max_rel=" + std::to_string(lmax));
+    report("b200::learn_filter weights vs FP64 loop", wmax <= 1e-4 * wref,
+           "max_rel=" + std::to_string(wmax / wref));
+    close("b200::learn_filter reconstruction vs FP64 loop", rel_err(r.reconstruction.data, reco),
+          1e-3, 1e-2);
+  }
+
   // error text passes through unchanged
   try {
     Sinogram<float> bad = Sinogram<float>::planar(3, Detector1D::centered(8, 1.0));
