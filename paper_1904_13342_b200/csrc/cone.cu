@@ -994,18 +994,8 @@ void host_backproject(tg_cone_plan& p, uint64_t z0, uint64_t nz, uint64_t v0, ui
   const uint64_t np = p.n_proj, per_view = p.det.n_u * n_rows;
   const uint64_t nvox = p.vol.shape[0] * p.vol.shape[1] * nz;
   if (fdk) ensure_fdk_weights(p, use_parker);
-  // View chunks grow geometrically (np/32, doubling up to np/4): K1 starts
-  // after a short first H2D and then trails the copy engine (K1 per view is
-  // slightly slower than PCIe per view), and few late launches keep the
-  // slab read-modify-write passes down.
-  std::vector<uint64_t> cw0;  // chunk first views; cw0.back() == np
-  {
-    const uint64_t cap = std::max<uint64_t>(1, (np + 3) / 4);
-    uint64_t c = std::max<uint64_t>(1, std::min(cap, (np + 31) / 32));
-    for (uint64_t w = 0; w < np; w += c, c = std::min(cap, 2 * c)) cw0.push_back(w);
-    cw0.push_back(np);
-  }
-  const int n_chunks = int(cw0.size()) - 1;
+  const uint64_t chunk = std::max<uint64_t>(1, (np + 7) / 8);
+  const int n_chunks = int((np + chunk - 1) / chunk);
   float *d_band, *d_slab;
   {
     std::lock_guard<std::mutex> lk(p.mu);
@@ -1024,13 +1014,13 @@ void host_backproject(tg_cone_plan& p, uint64_t z0, uint64_t nz, uint64_t v0, ui
   HostPipe hp(n_chunks + n_parts);
   const float scale = fdk ? float(fdk_scale(p, use_parker)) : 1.0f;
   for (int c = 0; c < n_chunks; ++c) {
-    const uint64_t w0 = cw0[c], wn = cw0[c + 1] - w0;
+    const uint64_t w0 = uint64_t(c) * chunk, wn = std::min(chunk, np - w0);
     TG_CUDA(cudaMemcpyAsync(d_band + w0 * per_view, h_band + w0 * per_view,
                             wn * per_view * sizeof(float), cudaMemcpyHostToDevice, hp.xs));
     TG_CUDA(cudaEventRecord(hp.ev[c], hp.xs));
   }
   for (int c = 0; c < n_chunks; ++c) {
-    const uint64_t w0 = cw0[c], wn = cw0[c + 1] - w0;
+    const uint64_t w0 = uint64_t(c) * chunk, wn = std::min(chunk, np - w0);
     TG_CUDA(cudaStreamWaitEvent(hp.cs, hp.ev[c], 0));
     float* part = d_band + w0 * per_view;
     if (fdk) prefilter_impl(p, part, part, use_parker, v0, n_rows, w0, wn, hp.cs);
@@ -1039,7 +1029,7 @@ void host_backproject(tg_cone_plan& p, uint64_t z0, uint64_t nz, uint64_t v0, ui
   if (!split) {
     TG_CUDA(cudaMemcpyAsync(h_slab, d_slab, nvox * sizeof(float), cudaMemcpyDeviceToHost, hp.cs));
   } else {
-    const uint64_t w_tail = cw0[n_head];
+    const uint64_t w_tail = uint64_t(n_head) * chunk;
     for (int q = 0; q < n_parts; ++q) {
       const uint64_t zq = uint64_t(q) * pz, nq = std::min(pz, nz - zq);
       backproject_impl(p, z0 + zq, nq, v0, n_rows, d_band, d_slab + zq * plane, scale, 1, hp.cs,
