@@ -467,8 +467,10 @@ def main():
             "e2e": {"value": e2e_value, "unit": UNIT,
                     "h2d_bytes_per_step": e2e_h2d,
                     "d2h_bytes_per_step": e2e_d2h,
-                    "path": "tg_cone_backproject_slab_host (pinned host band -> device, chunked "
-                            "H2D overlapped with K1, D2H of the slab)", "max_rel_diff_vs_device": e2e_parity,
+                    "path": "tg_cone_backproject_slab_host (pinned host band -> device; "
+                            "centre-out z phases: each ring uploads only its new detector rows "
+                            "in view chunks overlapped with K1, finished rings download while "
+                            "later rings upload)", "max_rel_diff_vs_device": e2e_parity,
                     "ms_per_step": 1e3 * e2e_s / e2e_n, "pcie": pcie},
             "fp": {"metric": "cone forward projection Gsamples/s (c4, Shepp-Logan)",
                    "value": fp_value, "unit": "Gsamples/s", "ms": fp_ms, "samples": fp_samples,

@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <memory>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -981,6 +982,11 @@ float* ensure_buffer(float*& buf, size_t& have, size_t need) {
   return buf;
 }
 
+void slab_rows(const tg_cone_geometry& g, uint64_t z0, uint64_t nz, uint64_t* v0,
+               uint64_t* n_rows);
+void phased_backproject(tg_cone_plan& p, uint64_t z0, uint64_t nz, uint64_t v0, uint64_t n_rows,
+                        const float* h_band, float* h_slab, float* d_band, float* d_slab);
+
 // Host-buffer back-projection / FDK of z-slab [z0, z0+nz) from detector rows
 // [v0, v0+n_rows) of every view (h_band [n_proj][n_rows][n_u] -> h_slab).
 // Views travel in ~8 chunks on a copy stream; K3 (FDK) and K1 of chunk c run
@@ -1001,6 +1007,10 @@ void host_backproject(tg_cone_plan& p, uint64_t z0, uint64_t nz, uint64_t v0, ui
     std::lock_guard<std::mutex> lk(p.mu);
     d_band = ensure_buffer(p.d_stage_in, p.stage_in_elems, np * per_view);
     d_slab = ensure_buffer(p.d_stage_out, p.stage_out_elems, nvox);
+  }
+  if (!fdk && nz >= 128 && np >= 8) {
+    phased_backproject(p, z0, nz, v0, n_rows, h_band, h_slab, d_band, d_slab);
+    return;
   }
   // The device-to-host copy of the slab overlaps the last views' K1: the
   // final two view chunks are back-projected z-part by z-part (32-aligned,
@@ -1082,6 +1092,125 @@ void slab_rows(const tg_cone_geometry& g, uint64_t z0, uint64_t nz, uint64_t* v0
   }
   *v0 = uint64_t(lo);
   *n_rows = uint64_t(hi - lo + 1);
+}
+
+// Back-projection from host buffers with the upload ordered centre-out in z.
+// No voxel is final before its last view has arrived, so a view-ordered
+// upload leaves the whole download (0.54 GB at c4) behind the last byte of the
+// upload.  Here the middle 64 slices' detector rows go first (all views, in 4
+// view chunks, each chunk back-projected as it lands), then four rings of
+// slices below and above, each uploading only the rows it needs beyond those
+// already resident (rows are monotone in z).  A ring's slices are final after
+// its last chunk and download while the next rings upload; the last ring's
+// final chunk runs per 32-slice part so its download starts part by part.
+// The centre rows are few (the cone is narrowest there), so K1 starts after a
+// short upload and then trails the copy engine.  Parts are 32-aligned from the
+// slab start: every K1 tile is the one the whole-slab launch would run.
+void phased_backproject(tg_cone_plan& p, uint64_t z0, uint64_t nz, uint64_t v0, uint64_t n_rows,
+                        const float* h_band, float* h_slab, float* d_band, float* d_slab) {
+  struct Range {
+    uint64_t z, n;  // slab-relative slices
+  };
+  const uint64_t np = p.n_proj, nu = p.det.n_u;
+  const uint64_t plane = p.vol.shape[0] * p.vol.shape[1];
+  const uint64_t units = (nz + 31) / 32;
+  auto slices = [&](uint64_t u0, uint64_t u1) {  // unit range -> slice range (clipped)
+    const uint64_t a = u0 * 32, b = std::min(nz, u1 * 32);
+    return Range{a, b > a ? b - a : 0};
+  };
+  std::vector<std::vector<Range>> phases;
+  // schedule knobs (experiments; defaults measured best at c4)
+  auto knob = [](const char* name, int dflt) {
+    const char* e = std::getenv(name);
+    return e ? std::max(1, std::atoi(e)) : dflt;
+  };
+  const uint64_t centre = std::min<uint64_t>(units, uint64_t(knob("TG_E2E_CENTRE_UNITS", 2)));
+  const uint64_t lo_u = (units - centre) / 2, hi_u = lo_u + centre;
+  phases.push_back({slices(lo_u, hi_u)});
+  const uint64_t below = lo_u, above = units - hi_u;
+  const int kRings = knob("TG_E2E_RINGS", 4);
+  for (int r = 0; r < kRings; ++r) {
+    const uint64_t b0 = below * r / kRings, b1 = below * (r + 1) / kRings;
+    const uint64_t a0 = above * r / kRings, a1 = above * (r + 1) / kRings;
+    std::vector<Range> ph;
+    if (b1 > b0) ph.push_back(slices(lo_u - b1, lo_u - b0));
+    if (a1 > a0) ph.push_back(slices(hi_u + a0, hi_u + a1));
+    if (!ph.empty()) phases.push_back(ph);
+  }
+  const tg_cone_geometry g{p.vol, p.det, p.n_proj, p.range, p.sid, p.sdd, p.mats.data(),
+                           p.sources.data(), p.invs.data(), p.angles.data()};
+  const int kChunks = knob("TG_E2E_CHUNKS", 4);
+  const uint64_t chunk = (np + kChunks - 1) / kChunks;
+  const int n_chunks = int((np + chunk - 1) / chunk);
+  const int n_phases = int(phases.size());
+  HostPipe hp(n_phases * n_chunks + n_phases + int(units) + 1);
+  cudaStream_t ds;  // downloads: concurrent with the uploads on xs
+  TG_CUDA(cudaStreamCreateWithFlags(&ds, cudaStreamNonBlocking));
+  int ev = 0;
+  uint64_t tlo = 0, thi = 0;  // resident rows (absolute), empty at first
+  const uint64_t row_bytes = nu * sizeof(float), view_pitch = n_rows * row_bytes;
+  auto download = [&](const Range& r) {
+    TG_CUDA(cudaMemcpyAsync(h_slab + r.z * plane, d_slab + r.z * plane, r.n * plane * sizeof(float),
+                            cudaMemcpyDeviceToHost, ds));
+  };
+  for (int ph = 0; ph < n_phases; ++ph) {
+    // rows this phase needs, clamped to the caller's band
+    uint64_t ra = ~0ull, rb = 0;
+    for (const Range& r : phases[ph]) {
+      uint64_t a = 0, n = 0;
+      slab_rows(g, z0 + r.z, r.n, &a, &n);
+      ra = std::min(ra, a);
+      rb = std::max(rb, a + n);
+    }
+    ra = std::max(ra, v0);
+    rb = std::min(rb, v0 + n_rows);
+    std::vector<std::pair<uint64_t, uint64_t>> segs;  // new rows [a, b)
+    if (thi <= tlo) {
+      if (rb > ra) segs.push_back({ra, rb});
+      tlo = ra;
+      thi = rb;
+    } else {
+      if (ra < tlo) segs.push_back({ra, tlo});
+      if (rb > thi) segs.push_back({thi, rb});
+      tlo = std::min(tlo, ra);
+      thi = std::max(thi, rb);
+    }
+    const bool last = ph == n_phases - 1;
+    for (int c = 0; c < n_chunks; ++c) {
+      const uint64_t w0 = uint64_t(c) * chunk, wn = std::min(chunk, np - w0);
+      for (const auto& sg : segs) {
+        const uint64_t off = (w0 * n_rows + (sg.first - v0)) * nu;
+        TG_CUDA(cudaMemcpy2DAsync(d_band + off, view_pitch, h_band + off, view_pitch,
+                                  (sg.second - sg.first) * row_bytes, wn, cudaMemcpyHostToDevice,
+                                  hp.xs));
+      }
+      TG_CUDA(cudaEventRecord(hp.ev[ev], hp.xs));
+      TG_CUDA(cudaStreamWaitEvent(hp.cs, hp.ev[ev++], 0));
+      if (last && c == n_chunks - 1) {
+        for (const Range& r : phases[ph])
+          for (uint64_t q = 0; q < r.n; q += 32) {
+            const Range part{r.z + q, std::min<uint64_t>(32, r.n - q)};
+            backproject_impl(p, z0 + part.z, part.n, v0, n_rows, d_band, d_slab + part.z * plane,
+                             1.0f, c > 0, hp.cs, w0, wn);
+            TG_CUDA(cudaEventRecord(hp.ev[ev], hp.cs));
+            TG_CUDA(cudaStreamWaitEvent(ds, hp.ev[ev++], 0));
+            download(part);
+          }
+      } else {
+        for (const Range& r : phases[ph])
+          backproject_impl(p, z0 + r.z, r.n, v0, n_rows, d_band, d_slab + r.z * plane, 1.0f,
+                           c > 0, hp.cs, w0, wn);
+      }
+    }
+    if (!last) {
+      TG_CUDA(cudaEventRecord(hp.ev[ev], hp.cs));
+      TG_CUDA(cudaStreamWaitEvent(ds, hp.ev[ev++], 0));
+      for (const Range& r : phases[ph]) download(r);
+    }
+  }
+  TG_CUDA(cudaStreamSynchronize(ds));
+  TG_CUDA(cudaStreamSynchronize(hp.cs));
+  cudaStreamDestroy(ds);
 }
 
 }  // namespace

@@ -1,0 +1,60 @@
+"""Time the c4 host-buffer back-projection (tg_cone_backproject_slab_host, the
+bench's e2e leg) under the TG_E2E_* schedule knobs of csrc/cone.cu
+phased_backproject (one variant per process).  Prints one JSON line each.
+
+    python scripts/e2e_variants.py --sweep
+"""
+import json
+import os
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def one():
+    import torch
+    import bench
+    import paper_1904_13342_b200 as tg
+    from paper_1904_13342_b200 import distributed as D
+    dev = torch.device("cuda", 0)
+    geo = bench.c4_geometry(tg)
+    me = D.slab_shards(geo, 1)[0]
+    band = bench.bump_band(torch, bench.C4["views"], me.v0, me.n_rows, bench.C4["nu"], dev)
+    h_band = torch.empty(band.shape, dtype=torch.float32, pin_memory=True)
+    h_band.copy_(band.cpu())
+    h_slab = torch.empty((me.nz, 512, 512), dtype=torch.float32, pin_memory=True)
+    L = tg._native.lib()
+    plan = geo._plan(0)
+
+    def step():
+        tg._native.check(L.tg_cone_backproject_slab_host(plan, me.z0, me.nz, me.v0, me.n_rows,
+                                                         h_band.data_ptr(), h_slab.data_ptr(), 0, 1))
+    for _ in range(2):
+        step()
+    ts = []
+    for _ in range(5):
+        t0 = time.perf_counter()
+        step()
+        ts.append(time.perf_counter() - t0)
+    ms = 1e3 * sorted(ts)[len(ts) // 2]
+    print(json.dumps({k: os.environ.get(k, "default") for k in
+                      ("TG_E2E_CENTRE_UNITS", "TG_E2E_RINGS", "TG_E2E_CHUNKS")} |
+                     {"ms_med": ms, "ms_min": 1e3 * min(ts),
+                      "gups": 512 ** 3 * 496 / (ms / 1e3) / 1e9}), flush=True)
+
+
+def sweep():
+    # round-1 sweep: centre {1,2,4} x rings {2,4,6,8} x chunks {4,8,16} -> 2/4/4 best
+    # (45.9 ms vs 47.0 at 8 chunks, 50-55 ms at 16); then chunks {2,3,4} x rings {3,4,5}
+    for c in ["2"]:
+        for r in ["3", "4", "5"]:
+            for ch in ["2", "3", "4"]:
+                env = dict(os.environ, TG_E2E_CENTRE_UNITS=c, TG_E2E_RINGS=r, TG_E2E_CHUNKS=ch)
+                subprocess.run([sys.executable, os.path.abspath(__file__)], env=env, timeout=300)
+
+
+if __name__ == "__main__":
+    sweep() if "--sweep" in sys.argv else one()
