@@ -378,7 +378,8 @@ def main():
     e2e_s = max_over_ranks(time.perf_counter() - t0)
     e2e_value = updates_total * e2e_n / e2e_s / 1e9
     # the host call back-projects with scale 1; the timed K1 carried the FDK constant
-    e2e_h2d = int(h_band.numel() * 4) * world
+    # bytes actually shipped host -> device per step (each view's own footprint)
+    e2e_h2d = int(L.tg_cone_last_h2d_bytes(plan)) * world
     e2e_d2h = int(h_slab.numel() * 4) * world
     e2e_parity = float((h_slab.to(dev) * scale - slab).abs().max() / slab.abs().max().clamp_min(1e-30))
     # PCIe copy rates on this box (pinned, one DMA each) to explain e2e
@@ -469,8 +470,9 @@ def main():
                     "d2h_bytes_per_step": e2e_d2h,
                     "path": "tg_cone_backproject_slab_host (pinned host band -> device; "
                             "centre-out z phases: each ring uploads only its new detector rows "
-                            "in view chunks overlapped with K1, finished rings download while "
-                            "later rings upload)", "max_rel_diff_vs_device": e2e_parity,
+                            "of each view's own footprint (3D copies per 8-view group) in view "
+                            "chunks overlapped with K1, finished rings download while later "
+                            "rings upload)", "host_band_bytes": int(h_band.numel() * 4), "max_rel_diff_vs_device": e2e_parity,
                     "ms_per_step": 1e3 * e2e_s / e2e_n, "pcie": pcie},
             "fp": {"metric": "cone forward projection Gsamples/s (c4, Shepp-Logan)",
                    "value": fp_value, "unit": "Gsamples/s", "ms": fp_ms, "samples": fp_samples,

@@ -189,6 +189,9 @@ tg_status tg_cone_fdk_host(tg_cone_plan* plan, const float* h_sino, float* h_vol
 tg_status tg_cone_backproject_slab_host(tg_cone_plan* plan, uint64_t z0, uint64_t nz, uint64_t v0,
                                         uint64_t n_rows, const float* h_band, float* h_slab,
                                         int fdk, int use_parker);
+/* bytes the plan's last host-buffer back-projection / FDK call copied host ->
+ * device (the slab-BP path ships each view's own detector footprint only) */
+uint64_t tg_cone_last_h2d_bytes(const tg_cone_plan* plan);
 
 /* ---- parallel / fan beam 2D (K4-K7) ------------------------------------ */
 

@@ -87,6 +87,7 @@ SIGNATURES = {
     "tg_cone_fdk_host": (c_int, [c_vp, c_vp, c_vp, c_int]),
     "tg_cone_backproject_slab_host": (c_int, [c_vp, c_u64, c_u64, c_u64, c_u64, c_vp, c_vp, c_int,
                                               c_int]),
+    "tg_cone_last_h2d_bytes": (c_u64, [c_vp]),
     "tg_planar_plan_create": (c_int, [_P(tg_planar_geometry), c_int, _P(c_vp)]),
     "tg_planar_plan_destroy": (c_int, [c_vp]),
     "tg_planar_forward": (c_int, [c_vp, c_vp, c_vp, c_vp]),
