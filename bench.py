@@ -380,6 +380,7 @@ def main():
     # the host call back-projects with scale 1; the timed K1 carried the FDK constant
     # bytes actually shipped host -> device per step (each view's own footprint)
     e2e_h2d = int(L.tg_cone_last_h2d_bytes(plan)) * world
+    e2e_band_bytes = int(h_band.numel() * 4) * world
     e2e_d2h = int(h_slab.numel() * 4) * world
     e2e_parity = float((h_slab.to(dev) * scale - slab).abs().max() / slab.abs().max().clamp_min(1e-30))
     # PCIe copy rates on this box (pinned, one DMA each) to explain e2e
@@ -472,7 +473,7 @@ def main():
                             "centre-out z phases: each ring uploads only its new detector rows "
                             "of each view's own footprint (3D copies per 8-view group) in view "
                             "chunks overlapped with K1, finished rings download while later "
-                            "rings upload)", "host_band_bytes": int(h_band.numel() * 4), "max_rel_diff_vs_device": e2e_parity,
+                            "rings upload)", "host_band_bytes": e2e_band_bytes, "max_rel_diff_vs_device": e2e_parity,
                     "ms_per_step": 1e3 * e2e_s / e2e_n, "pcie": pcie},
             "fp": {"metric": "cone forward projection Gsamples/s (c4, Shepp-Logan)",
                    "value": fp_value, "unit": "Gsamples/s", "ms": fp_ms, "samples": fp_samples,

@@ -1100,7 +1100,7 @@ void slab_rows(const tg_cone_geometry& g, uint64_t z0, uint64_t nz, uint64_t* v0
 // No voxel is final before its last view has arrived, so a view-ordered
 // upload leaves the whole download (0.54 GB at c4) behind the last byte of the
 // upload.  Here the middle 64 slices' detector rows go first (all views, in 4
-// view chunks, each chunk back-projected as it lands), then four rings of
+// view chunks, each chunk back-projected as it lands), then two rings of
 // slices below and above, each uploading only the rows it needs beyond those
 // already resident (rows are monotone in z).  A ring's slices are final after
 // its last chunk and download while the next rings upload; the last ring's
@@ -1130,7 +1130,7 @@ void phased_backproject(tg_cone_plan& p, uint64_t z0, uint64_t nz, uint64_t v0, 
   const uint64_t lo_u = (units - centre) / 2, hi_u = lo_u + centre;
   phases.push_back({slices(lo_u, hi_u)});
   const uint64_t below = lo_u, above = units - hi_u;
-  const int kRings = knob("TG_E2E_RINGS", 4);
+  const int kRings = knob("TG_E2E_RINGS", 2);
   for (int r = 0; r < kRings; ++r) {
     const uint64_t b0 = below * r / kRings, b1 = below * (r + 1) / kRings;
     const uint64_t a0 = above * r / kRings, a1 = above * (r + 1) / kRings;

@@ -41,7 +41,8 @@ def one():
         ts.append(time.perf_counter() - t0)
     ms = 1e3 * sorted(ts)[len(ts) // 2]
     print(json.dumps({k: os.environ.get(k, "default") for k in
-                      ("TG_E2E_CENTRE_UNITS", "TG_E2E_RINGS", "TG_E2E_CHUNKS")} |
+                      ("TG_E2E_CENTRE_UNITS", "TG_E2E_RINGS", "TG_E2E_CHUNKS", "TG_E2E_GROUP")} |
+                     {"h2d_bytes": int(L.tg_cone_last_h2d_bytes(plan))} |
                      {"ms_med": ms, "ms_min": 1e3 * min(ts),
                       "gups": 512 ** 3 * 496 / (ms / 1e3) / 1e9}), flush=True)
 
@@ -49,11 +50,15 @@ def one():
 def sweep():
     # round-1 sweep: centre {1,2,4} x rings {2,4,6,8} x chunks {4,8,16} -> 2/4/4 best
     # (45.9 ms vs 47.0 at 8 chunks, 50-55 ms at 16); then chunks {2,3,4} x rings {3,4,5}
-    for c in ["2"]:
-        for r in ["3", "4", "5"]:
-            for ch in ["2", "3", "4"]:
-                env = dict(os.environ, TG_E2E_CENTRE_UNITS=c, TG_E2E_RINGS=r, TG_E2E_CHUNKS=ch)
-                subprocess.run([sys.executable, os.path.abspath(__file__)], env=env, timeout=300)
+    # footprint uploads (1.41 GB instead of 2.09): K1 rather than PCIe bounds the
+    # pipeline, so re-sweep toward fewer phases / chunks and the copy group size
+    for c, r, ch, g in [("2", "4", "4", "8"), ("1", "4", "4", "8"), ("2", "2", "4", "8"),
+                        ("2", "3", "4", "8"), ("2", "2", "2", "8"), ("2", "3", "2", "8"),
+                        ("4", "2", "2", "8"), ("2", "4", "2", "8"), ("2", "1", "4", "8"),
+                        ("2", "4", "4", "2"), ("2", "4", "4", "31")]:
+        env = dict(os.environ, TG_E2E_CENTRE_UNITS=c, TG_E2E_RINGS=r, TG_E2E_CHUNKS=ch,
+                   TG_E2E_GROUP=g)
+        subprocess.run([sys.executable, os.path.abspath(__file__)], env=env, timeout=300)
 
 
 if __name__ == "__main__":
