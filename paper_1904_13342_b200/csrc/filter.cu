@@ -152,10 +152,18 @@ RowFilter* create(uint64_t n, uint64_t P, const double* weights, int device) {
   f->device = device;
   f->n = n;
   f->P = P;
-  for (uint64_t k = 1; k < P; ++k)
-    if (weights[k] != weights[P - k]) f->symmetric = false;
+  // filter_rows keeps Re(IFFT(W X)) of a real row (filtering.hpp:104-107),
+  // which equals IFFT(W_s X) with the symmetrised weights
+  // W_s[k] = (W[k] + W[P-k]) / 2 for any real W.  Symmetrising in FP64 makes
+  // every filter eligible for the two-rows-per-complex-FFT packing; without
+  // it the Ram-Lak window, symmetric in exact arithmetic but not bitwise after
+  // its FP64 FFT, fell back to one row per transform (2x the K3 work).
+  f->symmetric = true;
   std::vector<float> w(P);
-  for (uint64_t k = 0; k < P; ++k) w[k] = float(weights[k]);
+  // same rounding as symmetrize_kernel (the graph's trainable weights): the
+  // fp32 weights averaged in FP64
+  for (uint64_t k = 0; k < P; ++k)
+    w[k] = float(0.5 * (double(float(weights[k])) + double(float(weights[(P - k) & (P - 1)]))));
   std::vector<float2> tw(P);
   for (uint64_t k = 0; k < P; ++k) {
     const double ang = -2.0 * kPi * double(k) / double(P);

@@ -13,7 +13,7 @@ struct RowFilter {
   int device = 0;
   uint64_t n = 0;          // row length (detector bins)
   uint64_t P = 0;          // power-of-two window
-  bool symmetric = true;   // W[k] == W[P-k]: two real rows share one complex FFT
+  bool symmetric = true;   // weights symmetrised at creation: two real rows share one complex FFT
   float* d_w = nullptr;    // P real weights (fp32)
   float2* d_tw = nullptr;  // P twiddles exp(-2 pi i k / P) (from FP64)
   float2* d_tw16 = nullptr;  // per-pass [r][k] twiddle tables of the radix-16 path

@@ -140,7 +140,11 @@ def test_learn_filter_loop_matches_graph(tg):
     cfg = tg.ExperimentConfig(learning_rate=1.5e-5, iterations=12, filter_window=64)
     a = tg.learn_filter(sino, geo, cfg)
     b = tg.learn_filter(sino, geo, cfg, via_graph=True)
-    np.testing.assert_allclose(a.loss_history, b.loss_history, rtol=2e-6)
+    # the loss is |recon - target|^2 with recon close to target: fp32 rounding
+    # differences of the two summation orders are amplified by the
+    # cancellation (measured up to 8.5e-6 relative once the FBP target moved
+    # to the packed two-rows-per-FFT filter)
+    np.testing.assert_allclose(a.loss_history, b.loss_history, rtol=2e-5)
     np.testing.assert_allclose(a.learned_weights, b.learned_weights, rtol=1e-6,
                                atol=1e-7 * np.abs(b.learned_weights).max())
     # run-to-run determinism of the captured loop
