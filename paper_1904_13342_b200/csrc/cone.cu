@@ -1009,7 +1009,7 @@ void host_backproject(tg_cone_plan& p, uint64_t z0, uint64_t nz, uint64_t v0, ui
     d_band = ensure_buffer(p.d_stage_in, p.stage_in_elems, np * per_view);
     d_slab = ensure_buffer(p.d_stage_out, p.stage_out_elems, nvox);
   }
-  if (!fdk && nz >= 128 && np >= 8) {
+  if (!fdk && np >= 8) {
     phased_backproject(p, z0, nz, v0, n_rows, h_band, h_slab, d_band, d_slab);
     return;
   }

@@ -197,12 +197,14 @@ def test_cone_host_phased_upload(tg, O):
     assert_close(slab, dev[z0:z0 + nz], what="phased host slab vs device volume")
 
 
-def test_cone_host_footprint_upload(tg, O):
+@pytest.mark.parametrize("z0,nz", [(0, 160), (32, 64), (96, 40)])
+def test_cone_host_footprint_upload(tg, O, z0, nz):
     """the phased host back-projection ships each view's own detector footprint
     only (csrc/cone.cu phased_backproject): detector pixels outside the taps any
     voxel interpolates may hold anything (NaN here, on the host and left over in
     the device staging buffer from a previous call) without changing a bit of
-    the result, and fewer bytes than the band cross PCIe"""
+    the result, and fewer bytes than the band cross PCIe; whole volume and
+    z-slabs (the 64-slice slab is the N = 8 bench shard's shape)"""
     vol = tg.VolumeSpec.centered([40, 36, 160], [1.0, 1.0, 1.0])
     det = tg.Detector2D.centered(200, 260, 1.5, 1.5)
     geo = tg.make_cone(vol, det, 24, 2 * math.pi, 300.0, 600.0)
@@ -211,7 +213,7 @@ def test_cone_host_footprint_upload(tg, O):
     M = np.asarray(geo.matrices, np.float64).reshape(-1, 3, 4)
     xs = vol.origin[0] + np.arange(40) * 1.0
     ys = vol.origin[1] + np.arange(36) * 1.0
-    zs = vol.origin[2] + np.arange(160) * 1.0
+    zs = vol.origin[2] + np.arange(z0, z0 + nz) * 1.0
     Z, Y, X = np.meshgrid(zs, ys, xs, indexing="ij")
     pts = np.stack([X.ravel(), Y.ravel(), Z.ravel(), np.ones(X.size)])
     used = np.zeros(sino.shape, bool)
@@ -224,19 +226,21 @@ def test_cone_host_footprint_upload(tg, O):
                 ok = (uu >= 0) & (uu < 200) & (vv >= 0) & (vv < 260)
                 used[i, vv[ok], uu[ok]] = True
     assert used.mean() < 0.6
-    want = _bp(tg, geo, sino)
-    dirty = np.where(used, sino, np.float32(np.nan)).astype(np.float32)
+    v0, nr = tg.cone_slab_rows(geo, z0, nz)
+    band = np.ascontiguousarray(sino[:, v0:v0 + nr, :])
+    want = tg.cone_backproject_slab(geo, torch.from_numpy(band).to(DEV), z0, nz, v0).cpu().numpy()
+    dirty = np.ascontiguousarray(np.where(used, sino, np.float32(np.nan))[:, v0:v0 + nr, :])
     L = tg._native.lib()
     plan = geo._plan(0)
-    nan_vol = np.zeros((160, 36, 40), np.float32)
-    all_nan = np.full(sino.shape, np.nan, np.float32)
-    tg._native.check(L.tg_cone_backproject_slab_host(plan, 0, 160, 0, 260, all_nan.ctypes.data,
+    nan_vol = np.zeros((nz, 36, 40), np.float32)
+    all_nan = np.full(band.shape, np.nan, np.float32)
+    tg._native.check(L.tg_cone_backproject_slab_host(plan, z0, nz, v0, nr, all_nan.ctypes.data,
                                                      nan_vol.ctypes.data, 0, 0))
     assert np.isnan(nan_vol).any()
-    out = np.zeros((160, 36, 40), np.float32)
-    tg._native.check(L.tg_cone_backproject_slab_host(plan, 0, 160, 0, 260, dirty.ctypes.data,
+    out = np.zeros((nz, 36, 40), np.float32)
+    tg._native.check(L.tg_cone_backproject_slab_host(plan, z0, nz, v0, nr, dirty.ctypes.data,
                                                      out.ctypes.data, 0, 0))
     assert np.isfinite(out).all()
-    assert_close(out, want, 2e-7, 2e-6, "footprint-upload host BP vs device")
+    assert_close(out, want, 2e-7, 2e-6, "footprint-upload host slab BP vs device slab BP")
     shipped = int(L.tg_cone_last_h2d_bytes(plan))
-    assert 0 < shipped < 0.7 * sino.nbytes
+    assert 0 < shipped < 0.7 * band.nbytes
