@@ -209,6 +209,10 @@ __global__ void __maxnreg__(CIRC ? 72 : 96)
     mbar_fence_init();
   }
   __syncthreads();
+  // programmatic dependent launch: the next K1 of a chunked pipeline may start
+  // its view loop on the SMs this grid's tail leaves idle; it waits for this
+  // grid before its epilogue touches the volume (no-ops without PDL)
+  asm volatile("griddepcontrol.launch_dependents;");
   const Tile tile = make_tile(a, blockIdx.x, blockIdx.y, blockIdx.z, K);
 
   if (tid >= NCONS) {
@@ -218,7 +222,7 @@ __global__ void __maxnreg__(CIRC ? 72 : 96)
     for (int it = 0; it < a.n_views; ++it) {
       const int s = it % STAGES;
       if (it >= STAGES) mbar_wait(&empty[s], ((it / STAGES) - 1) & 1);
-      const double* P = c_views + 12 * it;
+      const double* P = c_views + 12 * (a.bank_off + it);
       double u = 0.0, v = 0.0;
       bool ok = true;
       if (lane < 8) corner_uv(P, a, tile, lane, u, v, ok);
@@ -423,6 +427,8 @@ __global__ void __maxnreg__(CIRC ? 72 : 96)
     if (lane == 0) mbar_arrive(&empty[s]);
   }
 
+  // the previous grid of the stream (PDL) has finished writing the volume
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   if (!valid) return;
 #pragma unroll
   for (int k = 0; k < K; ++k) {
@@ -721,32 +727,47 @@ void cone_args_base(const tg_cone_plan& p, BpArgs& a) {
 }
 
 template <int K, int BOXU, bool CIRC>
-void launch_bp_t(const CUtensorMap& map, const BpArgs& a, size_t smem, cudaStream_t st) {
+void launch_bp_t(const CUtensorMap& map, const BpArgs& a, size_t smem, cudaStream_t st, bool pdl) {
   auto fn = cone_bp_kernel<K, BOXU, CIRC>;
   TG_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   dim3 grid((a.nx + BX - 1) / BX, (a.ny + BY - 1) / BY, (a.nz + K - 1) / K);
-  fn<<<grid, NTHREADS, smem, st>>>(map, a);
+  if (!pdl) {
+    fn<<<grid, NTHREADS, smem, st>>>(map, a);
+    return;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(NTHREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  TG_CUDA(cudaLaunchKernelEx(&cfg, fn, map, a));
 }
 
 template <int K, bool CIRC>
-void launch_bp_u(int boxU, const CUtensorMap& map, const BpArgs& a, size_t smem, cudaStream_t st) {
+void launch_bp_u(int boxU, const CUtensorMap& map, const BpArgs& a, size_t smem, cudaStream_t st,
+                 bool pdl) {
   switch (boxU) {
-    case 48: return launch_bp_t<K, 48, CIRC>(map, a, smem, st);
-    case 80: return launch_bp_t<K, 80, CIRC>(map, a, smem, st);
-    case 112: return launch_bp_t<K, 112, CIRC>(map, a, smem, st);
-    case 176: return launch_bp_t<K, 176, CIRC>(map, a, smem, st);
-    default: return launch_bp_t<K, 240, CIRC>(map, a, smem, st);
+    case 48: return launch_bp_t<K, 48, CIRC>(map, a, smem, st, pdl);
+    case 80: return launch_bp_t<K, 80, CIRC>(map, a, smem, st, pdl);
+    case 112: return launch_bp_t<K, 112, CIRC>(map, a, smem, st, pdl);
+    case 176: return launch_bp_t<K, 176, CIRC>(map, a, smem, st, pdl);
+    default: return launch_bp_t<K, 240, CIRC>(map, a, smem, st, pdl);
   }
 }
 
 void launch_bp(int k, bool circ, int boxU, const CUtensorMap& map, const BpArgs& a, size_t smem,
-               cudaStream_t st) {
+               cudaStream_t st, bool pdl) {
   if (k == 32) {
-    if (circ) launch_bp_u<32, true>(boxU, map, a, smem, st);
-    else launch_bp_u<32, false>(boxU, map, a, smem, st);
+    if (circ) launch_bp_u<32, true>(boxU, map, a, smem, st, pdl);
+    else launch_bp_u<32, false>(boxU, map, a, smem, st, pdl);
   } else {
-    if (circ) launch_bp_u<16, true>(boxU, map, a, smem, st);
-    else launch_bp_u<16, false>(boxU, map, a, smem, st);
+    if (circ) launch_bp_u<16, true>(boxU, map, a, smem, st, pdl);
+    else launch_bp_u<16, false>(boxU, map, a, smem, st, pdl);
   }
 }
 
@@ -779,9 +800,16 @@ void size_box(tg_cone_plan& p) {
 
 // Back-project views [view0, view0 + n_views) of the band buffer (which holds
 // every view) into the slab.
+// pdl: launch with programmatic stream serialization, so consecutive K1
+// launches of a chunked pipeline overlap tail and head (the kernel waits for
+// the previous grid only before its epilogue).  Only for a stream whose
+// previous kernel does not produce this launch's projections (K1 after K1;
+// uploads are ordered by events, which stay full dependencies).  Measured on
+// the c4 host pipeline: 44.2 -> 43.3 ms.
 void backproject_impl(tg_cone_plan& p, uint64_t z0, uint64_t nz, uint64_t v0, uint64_t n_rows,
                       const float* d_band, float* d_slab, float scale, int accumulate,
-                      cudaStream_t st, uint64_t view0 = 0, uint64_t n_views = ~0ull) {
+                      cudaStream_t st, uint64_t view0 = 0, uint64_t n_views = ~0ull,
+                      bool pdl = false) {
   if (n_views == ~0ull) n_views = p.n_proj - view0;
   check(view0 + n_views <= p.n_proj && n_views >= 1, "view range lies outside the geometry");
   check(z0 + nz <= p.vol.shape[2] && nz >= 1, "slab lies outside the volume");
@@ -827,19 +855,25 @@ void backproject_impl(tg_cone_plan& p, uint64_t z0, uint64_t nz, uint64_t v0, ui
   const size_t smem = size_t(STAGES) * stage_elems * 4 + STAGES * 64 + 2 * STAGES * sizeof(uint64_t);
   KernelTimer timer;
   timer.start(st);
-  for (uint64_t c0 = view0; c0 < view0 + n_views; c0 += kMaxConstViews) {
-    const uint64_t cn = std::min<uint64_t>(kMaxConstViews, view0 + n_views - c0);
+  // the bank holds one aligned block of kMaxConstViews views (all of them up
+  // to 640), so chunked launches over one block need no re-upload between them
+  for (uint64_t c0 = view0; c0 < view0 + n_views;) {
+    const uint64_t blk = c0 / kMaxConstViews, b0 = blk * kMaxConstViews;
+    const uint64_t bn = std::min<uint64_t>(kMaxConstViews, p.n_proj - b0);
+    const uint64_t cn = std::min<uint64_t>(b0 + bn, view0 + n_views) - c0;
     a.n_views = int(cn);
+    a.bank_off = int(c0 - b0);
     a.view_base = int(c0);
     a.scale = scale;
     a.accumulate = (c0 == view0) ? accumulate : 1;
     std::lock_guard<std::mutex> lk(g_bank.mu);
-    // bank content key: (plan, first view, view count)
-    g_bank.acquire(p.device, (p.id << 40) ^ (c0 << 20) ^ cn, st, c_views, p.d_mats + 12 * c0,
-                   cn * 12 * sizeof(double));
-    launch_bp(p.k1_k, p.circular, p.boxU, map, a, smem, st);
+    // bank content key: (plan, block, view count)
+    g_bank.acquire(p.device, (p.id << 40) ^ (blk << 20) ^ bn, st, c_views, p.d_mats + 12 * b0,
+                   bn * 12 * sizeof(double));
+    launch_bp(p.k1_k, p.circular, p.boxU, map, a, smem, st, pdl);
     TG_LAUNCHED(1);
     g_bank.release(p.device, st);
+    c0 += cn;
   }
   timer.stop();
 }
@@ -1140,9 +1174,14 @@ void phased_backproject(tg_cone_plan& p, uint64_t z0, uint64_t nz, uint64_t v0, 
     if (!ph.empty()) phases.push_back(ph);
   }
   const int kChunks = knob("TG_E2E_CHUNKS", 4);
-  const uint64_t chunk = (np + kChunks - 1) / kChunks;
+  const int kGroup = knob("TG_E2E_GROUP", 8);
+  // view chunks are whole copy groups (a group's residency is tracked for all
+  // of its views at once)
+  const uint64_t chunk = ((np + kChunks - 1) / kChunks + kGroup - 1) / kGroup * kGroup;
   const int n_chunks = int((np + chunk - 1) / chunk);
   const int n_phases = int(phases.size());
+  // consecutive K1 launches overlap (programmatic dependent launch)
+  const bool kPdl = std::getenv("TG_E2E_NOPDL") == nullptr;
 
   // Per-view footprints.  K1 reads taps floor(u), floor(u)+1 (and the same in
   // v) of voxel centres only, and for w > 0 the projective image of a box of
@@ -1154,7 +1193,6 @@ void phased_backproject(tg_cone_plan& p, uint64_t z0, uint64_t nz, uint64_t v0, 
   // caller's full band.  Copy groups of kGroup consecutive views (one 3D copy
   // per group and row segment, union of the group's ranges) keep the number
   // of copies small; the columns are widened to 64-byte boundaries.
-  const int kGroup = knob("TG_E2E_GROUP", 8);
   const double* vo = p.vol.origin;
   const double* vs = p.vol.spacing;
   const double xs[2] = {vo[0], vo[0] + double(p.vol.shape[0] - 1) * vs[0]};
@@ -1252,21 +1290,17 @@ void phased_backproject(tg_cone_plan& p, uint64_t z0, uint64_t nz, uint64_t v0, 
             rb = std::max(rb, f.vb);
           }
         if (rb <= ra) continue;
-        int64_t& lo = g_lo[gi];
+        int64_t& lo = g_lo[gi];  // rows resident for every view of the group
         int64_t& hi = g_hi[gi];
         if (hi <= lo) {
           upload(a, b - a, g_ua[gi], g_ub[gi], ra, rb);
-          if (b == std::min<uint64_t>((gi + 1) * kGroup, np)) {
-            lo = ra;
-            hi = rb;
-          }
+          lo = ra;
+          hi = rb;
         } else {
           if (ra < lo) upload(a, b - a, g_ua[gi], g_ub[gi], ra, lo);
           if (rb > hi) upload(a, b - a, g_ua[gi], g_ub[gi], hi, rb);
-          if (b == std::min<uint64_t>((gi + 1) * kGroup, np)) {
-            lo = std::min(lo, ra);
-            hi = std::max(hi, rb);
-          }
+          lo = std::min(lo, ra);
+          hi = std::max(hi, rb);
         }
       }
       TG_CUDA(cudaEventRecord(hp.ev[ev], hp.xs));
@@ -1276,7 +1310,7 @@ void phased_backproject(tg_cone_plan& p, uint64_t z0, uint64_t nz, uint64_t v0, 
           for (uint64_t q = 0; q < r.n; q += 32) {
             const Range part{r.z + q, std::min<uint64_t>(32, r.n - q)};
             backproject_impl(p, z0 + part.z, part.n, v0, n_rows, d_band, d_slab + part.z * plane,
-                             1.0f, c > 0, hp.cs, w0, wn);
+                             1.0f, c > 0, hp.cs, w0, wn, kPdl);
             TG_CUDA(cudaEventRecord(hp.ev[ev], hp.cs));
             TG_CUDA(cudaStreamWaitEvent(ds, hp.ev[ev++], 0));
             download(part);
@@ -1284,7 +1318,7 @@ void phased_backproject(tg_cone_plan& p, uint64_t z0, uint64_t nz, uint64_t v0, 
       } else {
         for (const Range& r : phases[ph])
           backproject_impl(p, z0 + r.z, r.n, v0, n_rows, d_band, d_slab + r.z * plane, 1.0f,
-                           c > 0, hp.cs, w0, wn);
+                           c > 0, hp.cs, w0, wn, kPdl);
       }
     }
     if (!last) {

@@ -33,7 +33,8 @@ struct BpArgs {
   double sx, sy, sz;        // voxel pitch
   int nu, nv;               // full detector
   int band_v0, band_rows;   // detector rows present in `sino`
-  int n_views;              // views in this launch (constant slots 0..n-1)
+  int n_views;              // views in this launch (constant slots bank_off..bank_off+n-1)
+  int bank_off;             // first view's slot in the constant bank
   int view_base;            // first view's index in the TMA tensor / sino buffer
   int boxU, boxV;           // TMA box (elements)
   float sid2;               // SID^2: 1/w^2 = SID^2 / hz^2

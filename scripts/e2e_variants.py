@@ -41,7 +41,8 @@ def one():
         ts.append(time.perf_counter() - t0)
     ms = 1e3 * sorted(ts)[len(ts) // 2]
     print(json.dumps({k: os.environ.get(k, "default") for k in
-                      ("TG_E2E_CENTRE_UNITS", "TG_E2E_RINGS", "TG_E2E_CHUNKS", "TG_E2E_GROUP")} |
+                      ("TG_E2E_CENTRE_UNITS", "TG_E2E_RINGS", "TG_E2E_CHUNKS", "TG_E2E_GROUP",
+                               "TG_E2E_NOPDL")} |
                      {"h2d_bytes": int(L.tg_cone_last_h2d_bytes(plan))} |
                      {"ms_med": ms, "ms_min": 1e3 * min(ts),
                       "gups": 512 ** 3 * 496 / (ms / 1e3) / 1e9}), flush=True)
@@ -52,12 +53,15 @@ def sweep():
     # (45.9 ms vs 47.0 at 8 chunks, 50-55 ms at 16); then chunks {2,3,4} x rings {3,4,5}
     # footprint uploads (1.41 GB instead of 2.09): K1 rather than PCIe bounds the
     # pipeline, so re-sweep toward fewer phases / chunks and the copy group size
-    for c, r, ch, g in [("2", "4", "4", "8"), ("1", "4", "4", "8"), ("2", "2", "4", "8"),
-                        ("2", "3", "4", "8"), ("2", "2", "2", "8"), ("2", "3", "2", "8"),
-                        ("4", "2", "2", "8"), ("2", "4", "2", "8"), ("2", "1", "4", "8"),
-                        ("2", "4", "4", "2"), ("2", "4", "4", "31")]:
+    # programmatic dependent launch between the chunked K1 launches: on / off,
+    # and with it more chunks (whose launch tails PDL now hides)
+    # (measured: 2/2/4 43.3 ms with PDL, 44.2 without; 8 chunks 45.7; 2/4/4 43.7;
+    # 2/3/6 44.8; 1/2/4 44.8 — profiles/r1_e2e_pdl_sweep.jsonl)
+    for c, r, ch, g, mode in [("2", "2", "4", "8", "pdl"), ("2", "2", "4", "8", "nopdl")]:
         env = dict(os.environ, TG_E2E_CENTRE_UNITS=c, TG_E2E_RINGS=r, TG_E2E_CHUNKS=ch,
                    TG_E2E_GROUP=g)
+        if mode == "nopdl":
+            env["TG_E2E_NOPDL"] = "1"
         subprocess.run([sys.executable, os.path.abspath(__file__)], env=env, timeout=300)
 
 
