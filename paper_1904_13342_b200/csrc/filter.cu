@@ -198,13 +198,19 @@ void destroy(RowFilter* f) {
   delete f;
 }
 
-// FDK pre-weights as one elementwise pass: one CTA per detector row (no
-// per-element index division), float4 loads / stores when rows are 16-byte
-// aligned; the FP64 products and their two fp32 roundings are the
-// reference's (filtering.hpp:136-154, applied cosine then Parker)
-__global__ void __launch_bounds__(256) preweight_kernel(const float* in, float* out, int n,
-                                                        PreWeights pw) {
-  const uint64_t row = blockIdx.x;
+// FDK pre-weights as one elementwise pass: one warp per detector row (no
+// per-element index division; 8 rows per CTA), float4 loads / stores when
+// rows are 16-byte aligned, each lane keeping two float4 in flight; the FP64
+// products and their two fp32 roundings are the reference's
+// (filtering.hpp:136-154, applied cosine then Parker).  One CTA of 256
+// threads per 312-float4 row left 56 threads with a second round: 1.2 ms at
+// c4's band.
+constexpr int kPwRows = 8;
+__global__ void __launch_bounds__(32 * kPwRows) preweight_kernel(const float* in, float* out, int n,
+                                                                 uint64_t n_rows, PreWeights pw) {
+  const uint64_t row = uint64_t(blockIdx.x) * kPwRows + (threadIdx.x >> 5);
+  if (row >= n_rows) return;
+  const int lane = threadIdx.x & 31;
   const float* src = in + row * uint64_t(n);
   float* dst = out + row * uint64_t(n);
   const double* cw = pw.cos ? pw.cos + (pw.cos_row0 + row % pw.rows_per_view) * uint64_t(n) : nullptr;
@@ -214,19 +220,27 @@ __global__ void __launch_bounds__(256) preweight_kernel(const float* in, float* 
     if (pk) v = float(double(v) * __ldg(pk + j));
     return v;
   };
+  auto weigh4 = [&](float4 v, int j) {
+    v.x = weigh(v.x, j);
+    v.y = weigh(v.y, j + 1);
+    v.z = weigh(v.z, j + 2);
+    v.w = weigh(v.w, j + 3);
+    return v;
+  };
   if ((n & 3) == 0 && (reinterpret_cast<uintptr_t>(src) & 15) == 0 &&
       (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
-    for (int c = threadIdx.x; c < n / 4; c += blockDim.x) {
-      float4 v = reinterpret_cast<const float4*>(src)[c];
-      const int j = 4 * c;
-      v.x = weigh(v.x, j);
-      v.y = weigh(v.y, j + 1);
-      v.z = weigh(v.z, j + 2);
-      v.w = weigh(v.w, j + 3);
-      reinterpret_cast<float4*>(dst)[c] = v;
+    const float4* s4 = reinterpret_cast<const float4*>(src);
+    float4* d4 = reinterpret_cast<float4*>(dst);
+    const int n4 = n / 4;
+    int c = lane;
+    for (; c + 32 < n4; c += 64) {
+      const float4 a = __ldcs(s4 + c), b = __ldcs(s4 + c + 32);
+      __stcs(d4 + c, weigh4(a, 4 * c));
+      __stcs(d4 + c + 32, weigh4(b, 4 * (c + 32)));
     }
+    if (c < n4) __stcs(d4 + c, weigh4(__ldcs(s4 + c), 4 * c));
   } else {
-    for (int j = threadIdx.x; j < n; j += blockDim.x) dst[j] = weigh(src[j], j);
+    for (int j = lane; j < n; j += 32) dst[j] = weigh(src[j], j);
   }
 }
 
@@ -248,7 +262,9 @@ void apply(const RowFilter& f, const float* d_in, float* d_out, uint64_t n_rows,
   const float* src = d_in;
   if (sep) {
     check(n_rows <= 2147483647ull, "too many detector rows for one filter launch");
-    preweight_kernel<<<unsigned(n_rows), 256, 0, st>>>(d_in, d_out, n, w);
+    const uint64_t pw_blocks = (n_rows + kPwRows - 1) / kPwRows;
+    check(pw_blocks <= 2147483647ull, "too many detector rows for one filter launch");
+    preweight_kernel<<<unsigned(pw_blocks), 32 * kPwRows, 0, st>>>(d_in, d_out, n, n_rows, w);
     TG_LAUNCHED(1);
     src = d_out;
     w = PreWeights{};

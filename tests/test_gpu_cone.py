@@ -244,3 +244,20 @@ def test_cone_host_footprint_upload(tg, O, z0, nz):
     assert_close(out, want, 2e-7, 2e-6, "footprint-upload host slab BP vs device slab BP")
     shipped = int(L.tg_cone_last_h2d_bytes(plan))
     assert 0 < shipped < 0.7 * band.nbytes
+
+
+def test_cone_many_views_bank_blocks(tg, O):
+    """more views than one constant-bank block (640): K1 launches split at the
+    aligned block boundary; the device path and the host pipeline (PDL-chained
+    chunk launches whose chunks start inside a block and straddle its end)
+    both match the oracle"""
+    geo, og = cone_pair(tg, O, [20, 18, 40], [1.0] * 3, 28, 48, 1.5, 1.5, 700, 2 * math.pi,
+                        150.0, 300.0)
+    s = rand(og.sino_shape, 12, -1.0, 1.0)
+    ref = O.cone_backproject(og, s)
+    dev = _bp(tg, geo, s)
+    assert_close(dev, ref, what="cone BP, 700 views (device)")
+    host = tg.back_project(tg.Sinogram.cone_beam(700, geo.detector, data=s), geo).data
+    assert_close(host, ref, what="cone BP, 700 views (host pipeline)")
+    # five partial fp32 sums (view chunks / bank blocks) instead of two
+    assert_close(host, dev, 1e-6, 2e-6, "host pipeline vs device, 700 views")
