@@ -242,6 +242,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-fdk-e2e", action="store_true",
+                    help="skip the FDK-from-host-sinogram leg (tg_cone_fdk_host)")
     ap.add_argument("--fp-steps", type=int, default=3)
     ap.add_argument("--c5-iters", type=int, default=2,
                     help="TV-loop iterations timed at config c5 (0 = skip the c5 leg)")
@@ -396,6 +398,37 @@ def main():
     pcie = {"h2d_gbs": h_band.numel() * 4 / (h2d_ms / 1e3) / 1e9, "h2d_ms": h2d_ms,
             "d2h_gbs": h_slab.numel() * 4 / (d2h_ms / 1e3) / 1e9, "d2h_ms": d2h_ms}
 
+    # ---- FDK end to end from a full host sinogram (the C++ drop-in's path) ----
+    # tg_cone_fdk_host: raw projections [496][960][1248] in pinned host memory ->
+    # volume in pinned host memory; only the volume's detector rows travel and
+    # are weighted / filtered (K3) before K1.  Rows outside the band are zero.
+    fdk_e2e = None
+    if world == 1 and not args.no_fdk_e2e:
+        h_sino = torch.zeros((C4["views"], C4["nv"], C4["nu"]), dtype=torch.float32,
+                             pin_memory=True)
+        h_sino[:, me.v0:me.v0 + me.n_rows].copy_(raw_band.cpu())
+        h_vol = torch.empty((C4["n"],) * 3, dtype=torch.float32, pin_memory=True)
+
+        def fdk_step():
+            tg._native.check(L.tg_cone_fdk_host(plan, h_sino.data_ptr(), h_vol.data_ptr(), 1))
+            return float(h_vol[0, 0, 0])
+
+        fdk_step()
+        t0 = time.perf_counter()
+        n_fdk = 3
+        for _ in range(n_fdk):
+            fdk_step()
+        fdk_s = (time.perf_counter() - t0) / n_fdk
+        fdk_parity = float((h_vol.to(dev) - slab).abs().max() / slab.abs().max().clamp_min(1e-30))
+        fdk_e2e = {"value": updates_total / fdk_s / 1e9, "unit": UNIT, "ms_per_step": 1e3 * fdk_s,
+                   "h2d_bytes_per_step": int(L.tg_cone_last_h2d_bytes(plan)),
+                   "d2h_bytes_per_step": int(h_vol.numel() * 4),
+                   "host_sinogram_bytes": int(h_sino.numel() * 4),
+                   "path": "tg_cone_fdk_host (pinned raw projections -> cosine x Parker + Ram-Lak "
+                           "(K3) -> K1 -> pinned volume; view chunks overlapped)",
+                   "max_rel_diff_vs_device": fdk_parity}
+        del h_sino, h_vol
+
     # ---- roofline (K1) --------------------------------------------------------
     pk = peaks()
     sm_max = float(pk.get("sm_max_mhz", 1965.0))
@@ -483,6 +516,7 @@ def main():
                    # scripts/k2_tex_bench.cu: the same gather pattern with ideal coherence
                    "measured_gather_ceiling_gsamples": 611.0,
                    "measured_gather_ceiling_frac": fp_value / 611.0},
+            "fdk_e2e": fdk_e2e,
             "k3_fdk_prefilter_ms": k3_ms, "k1_ms_mean": k1_avg, "k1_ms_min": min(k1_ms),
             # FDK of this rank's slab (pipelines.hpp:73-84): K3 on the band + K1
             "fdk_ms": k3_ms + k1_avg,

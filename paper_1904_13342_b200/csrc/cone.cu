@@ -1023,12 +1023,15 @@ void phased_backproject(tg_cone_plan& p, uint64_t z0, uint64_t nz, uint64_t v0, 
                         const float* h_band, float* h_slab, float* d_band, float* d_slab);
 
 // Host-buffer back-projection / FDK of z-slab [z0, z0+nz) from detector rows
-// [v0, v0+n_rows) of every view (h_band [n_proj][n_rows][n_u] -> h_slab).
-// Views travel in ~8 chunks on a copy stream; K3 (FDK) and K1 of chunk c run
-// while chunk c+1 is in flight, K1 accumulating chunk after chunk.  Device
-// staging buffers are owned by the plan and reused across calls.
+// [v0, v0+n_rows) of every view (h_band [n_proj][n_rows][n_u] -> h_slab; with
+// h_view_pitch > 0 the band's views sit h_view_pitch elements apart, e.g. the
+// rows of a full host sinogram).  Views travel in ~8 chunks on a copy stream;
+// K3 (FDK) and K1 of chunk c run while chunk c+1 is in flight, K1
+// accumulating chunk after chunk.  Device staging buffers are owned by the
+// plan and reused across calls.
 void host_backproject(tg_cone_plan& p, uint64_t z0, uint64_t nz, uint64_t v0, uint64_t n_rows,
-                      const float* h_band, float* h_slab, int fdk, bool use_parker) {
+                      const float* h_band, float* h_slab, int fdk, bool use_parker,
+                      uint64_t h_view_pitch = 0) {
   check(z0 + nz <= p.vol.shape[2] && nz >= 1, "slab lies outside the volume");
   check(n_rows >= 1 && v0 + n_rows <= p.det.n_v, "detector row band lies outside the detector");
   DeviceGuard dg(p.device);
@@ -1043,7 +1046,8 @@ void host_backproject(tg_cone_plan& p, uint64_t z0, uint64_t nz, uint64_t v0, ui
     d_band = ensure_buffer(p.d_stage_in, p.stage_in_elems, np * per_view);
     d_slab = ensure_buffer(p.d_stage_out, p.stage_out_elems, nvox);
   }
-  if (!fdk && np >= 8) {
+  if (h_view_pitch == 0) h_view_pitch = per_view;
+  if (!fdk && np >= 8 && h_view_pitch == per_view) {
     phased_backproject(p, z0, nz, v0, n_rows, h_band, h_slab, d_band, d_slab);
     return;
   }
@@ -1061,8 +1065,13 @@ void host_backproject(tg_cone_plan& p, uint64_t z0, uint64_t nz, uint64_t v0, ui
   p.last_h2d_bytes = np * per_view * sizeof(float);
   for (int c = 0; c < n_chunks; ++c) {
     const uint64_t w0 = uint64_t(c) * chunk, wn = std::min(chunk, np - w0);
-    TG_CUDA(cudaMemcpyAsync(d_band + w0 * per_view, h_band + w0 * per_view,
-                            wn * per_view * sizeof(float), cudaMemcpyHostToDevice, hp.xs));
+    if (h_view_pitch == per_view)
+      TG_CUDA(cudaMemcpyAsync(d_band + w0 * per_view, h_band + w0 * per_view,
+                              wn * per_view * sizeof(float), cudaMemcpyHostToDevice, hp.xs));
+    else
+      TG_CUDA(cudaMemcpy2DAsync(d_band + w0 * per_view, per_view * sizeof(float),
+                                h_band + w0 * h_view_pitch, h_view_pitch * sizeof(float),
+                                per_view * sizeof(float), wn, cudaMemcpyHostToDevice, hp.xs));
     TG_CUDA(cudaEventRecord(hp.ev[c], hp.xs));
   }
   for (int c = 0; c < n_chunks; ++c) {
@@ -1523,7 +1532,15 @@ uint64_t tg_cone_last_h2d_bytes(const tg_cone_plan* p) { return p ? p->last_h2d_
 
 tg_status tg_cone_fdk_host(tg_cone_plan* p, const float* h_sino, float* h_vol, int use_parker) {
   return guarded([&] {
-    host_backproject(*p, 0, p->vol.shape[2], 0, p->det.n_v, h_sino, h_vol, 1, use_parker != 0);
+    // FDK of the whole volume needs only the detector rows the volume
+    // projects onto (K3 filters along u within a row): the rest of each view
+    // is neither uploaded nor filtered
+    const tg_cone_geometry g{p->vol, p->det, p->n_proj, p->range, p->sid, p->sdd, p->mats.data(),
+                             p->sources.data(), p->invs.data(), p->angles.data()};
+    uint64_t v0 = 0, n_rows = p->det.n_v;
+    slab_rows(g, 0, p->vol.shape[2], &v0, &n_rows);
+    host_backproject(*p, 0, p->vol.shape[2], v0, n_rows, h_sino + v0 * p->det.n_u, h_vol, 1,
+                     use_parker != 0, p->det.n_v * p->det.n_u);
   });
 }
 
