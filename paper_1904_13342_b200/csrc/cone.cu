@@ -1038,8 +1038,24 @@ void host_backproject(tg_cone_plan& p, uint64_t z0, uint64_t nz, uint64_t v0, ui
   const uint64_t np = p.n_proj, per_view = p.det.n_u * n_rows;
   const uint64_t nvox = p.vol.shape[0] * p.vol.shape[1] * nz;
   if (fdk) ensure_fdk_weights(p, use_parker);
+  // View chunks: a geometric head (np/32, np/16, then np/8 each) so K3 / K1
+  // start after a short first upload (compute per view outpaces the copy
+  // engine from then on: c4 FDK 0.092 vs 0.076 ms per view), and two np/8
+  // chunks at the end, whose K1 runs per z-part while finished parts download.
   const uint64_t chunk = std::max<uint64_t>(1, (np + 7) / 8);
-  const int n_chunks = int((np + chunk - 1) / chunk);
+  std::vector<uint64_t> starts;
+  {
+    const uint64_t tail0 = np > 2 * chunk ? np - 2 * chunk : 0;
+    uint64_t w = 0, c = std::max<uint64_t>(1, (np + 31) / 32);
+    while (w < tail0) {
+      starts.push_back(w);
+      w += std::min(c, tail0 - w);
+      c = std::min(chunk, 2 * c);
+    }
+    for (uint64_t t = tail0; t < np; t += chunk) starts.push_back(t);
+    starts.push_back(np);
+  }
+  const int n_chunks = int(starts.size()) - 1;
   float *d_band, *d_slab;
   {
     std::lock_guard<std::mutex> lk(p.mu);
@@ -1064,7 +1080,7 @@ void host_backproject(tg_cone_plan& p, uint64_t z0, uint64_t nz, uint64_t v0, ui
   const float scale = fdk ? float(fdk_scale(p, use_parker)) : 1.0f;
   p.last_h2d_bytes = np * per_view * sizeof(float);
   for (int c = 0; c < n_chunks; ++c) {
-    const uint64_t w0 = uint64_t(c) * chunk, wn = std::min(chunk, np - w0);
+    const uint64_t w0 = starts[c], wn = starts[c + 1] - w0;
     if (h_view_pitch == per_view)
       TG_CUDA(cudaMemcpyAsync(d_band + w0 * per_view, h_band + w0 * per_view,
                               wn * per_view * sizeof(float), cudaMemcpyHostToDevice, hp.xs));
@@ -1075,7 +1091,7 @@ void host_backproject(tg_cone_plan& p, uint64_t z0, uint64_t nz, uint64_t v0, ui
     TG_CUDA(cudaEventRecord(hp.ev[c], hp.xs));
   }
   for (int c = 0; c < n_chunks; ++c) {
-    const uint64_t w0 = uint64_t(c) * chunk, wn = std::min(chunk, np - w0);
+    const uint64_t w0 = starts[c], wn = starts[c + 1] - w0;
     TG_CUDA(cudaStreamWaitEvent(hp.cs, hp.ev[c], 0));
     float* part = d_band + w0 * per_view;
     if (fdk) prefilter_impl(p, part, part, use_parker, v0, n_rows, w0, wn, hp.cs);
@@ -1084,11 +1100,13 @@ void host_backproject(tg_cone_plan& p, uint64_t z0, uint64_t nz, uint64_t v0, ui
   if (!split) {
     TG_CUDA(cudaMemcpyAsync(h_slab, d_slab, nvox * sizeof(float), cudaMemcpyDeviceToHost, hp.cs));
   } else {
-    const uint64_t w_tail = uint64_t(n_head) * chunk;
+    const uint64_t w_tail = starts[n_head];
     for (int q = 0; q < n_parts; ++q) {
       const uint64_t zq = uint64_t(q) * pz, nq = std::min(pz, nz - zq);
+      // parts after the first follow a K1, not the K3 producing their input:
+      // programmatic dependent launch overlaps their heads with its tail
       backproject_impl(p, z0 + zq, nq, v0, n_rows, d_band, d_slab + zq * plane, scale, 1, hp.cs,
-                       w_tail, np - w_tail);
+                       w_tail, np - w_tail, q > 0);
       TG_CUDA(cudaEventRecord(hp.ev[n_chunks + q], hp.cs));
       TG_CUDA(cudaStreamWaitEvent(hp.xs, hp.ev[n_chunks + q], 0));
       TG_CUDA(cudaMemcpyAsync(h_slab + zq * plane, d_slab + zq * plane, nq * plane * sizeof(float),
