@@ -974,7 +974,8 @@ void ensure_fdk_weights(tg_cone_plan& p, bool use_parker) {
 }
 
 void prefilter_impl(tg_cone_plan& p, const float* d_in, float* d_out, bool use_parker, uint64_t v0,
-                    uint64_t n_rows, uint64_t view0, uint64_t n_views, cudaStream_t st) {
+                    uint64_t n_rows, uint64_t view0, uint64_t n_views, cudaStream_t st,
+                    filt::RowLayout lay = filt::RowLayout{}) {
   check(n_rows >= 1 && v0 + n_rows <= p.det.n_v, "detector row band lies outside the detector");
   ensure_fdk_weights(p, use_parker);
   DeviceGuard dg(p.device);
@@ -983,7 +984,7 @@ void prefilter_impl(tg_cone_plan& p, const float* d_in, float* d_out, bool use_p
   pw.cos_row0 = v0;
   pw.rows_per_view = n_rows;
   pw.parker = use_parker ? p.d_parker + view0 * p.det.n_u : nullptr;
-  filt::apply(*p.ramlak, d_in, d_out, n_views * n_rows, &pw, st);
+  filt::apply(*p.ramlak, d_in, d_out, n_views * n_rows, &pw, st, lay);
 }
 
 double fdk_scale(const tg_cone_plan& p, bool use_parker) {  // pipelines.hpp:80-81
@@ -1020,7 +1021,8 @@ float* ensure_buffer(float*& buf, size_t& have, size_t need) {
 void slab_rows(const tg_cone_geometry& g, uint64_t z0, uint64_t nz, uint64_t* v0,
                uint64_t* n_rows);
 void phased_backproject(tg_cone_plan& p, uint64_t z0, uint64_t nz, uint64_t v0, uint64_t n_rows,
-                        const float* h_band, float* h_slab, float* d_band, float* d_slab);
+                        const float* h_band, float* h_slab, float* d_band, float* d_slab,
+                        uint64_t h_view_pitch, bool fdk, bool use_parker, float scale);
 
 // Host-buffer back-projection / FDK of z-slab [z0, z0+nz) from detector rows
 // [v0, v0+n_rows) of every view (h_band [n_proj][n_rows][n_u] -> h_slab; with
@@ -1063,8 +1065,13 @@ void host_backproject(tg_cone_plan& p, uint64_t z0, uint64_t nz, uint64_t v0, ui
     d_slab = ensure_buffer(p.d_stage_out, p.stage_out_elems, nvox);
   }
   if (h_view_pitch == 0) h_view_pitch = per_view;
-  if (!fdk && np >= 8 && h_view_pitch == per_view) {
-    phased_backproject(p, z0, nz, v0, n_rows, h_band, h_slab, d_band, d_slab);
+  // centre-out phased pipeline (BP: footprint uploads; FDK: whole rows, each
+  // new row segment weighted and filtered as it lands — needs the register
+  // FFT path of K3 for strided row segments)
+  if (np >= 8 && (!fdk || (p.ramlak->P >= 512 && p.ramlak->P <= 8192)) &&
+      std::getenv("TG_HOST_NOPHASE") == nullptr) {
+    phased_backproject(p, z0, nz, v0, n_rows, h_band, h_slab, d_band, d_slab, h_view_pitch, fdk != 0,
+                       use_parker, fdk ? float(fdk_scale(p, use_parker)) : 1.0f);
     return;
   }
   // The device-to-host copy of the slab overlaps the last views' K1: the
@@ -1170,7 +1177,8 @@ void slab_rows(const tg_cone_geometry& g, uint64_t z0, uint64_t nz, uint64_t* v0
 // short upload and then trails the copy engine.  Parts are 32-aligned from the
 // slab start: every K1 tile is the one the whole-slab launch would run.
 void phased_backproject(tg_cone_plan& p, uint64_t z0, uint64_t nz, uint64_t v0, uint64_t n_rows,
-                        const float* h_band, float* h_slab, float* d_band, float* d_slab) {
+                        const float* h_band, float* h_slab, float* d_band, float* d_slab,
+                        uint64_t h_view_pitch, bool fdk, bool use_parker, float scale) {
   struct Range {
     uint64_t z, n;  // slab-relative slices
   };
@@ -1207,8 +1215,12 @@ void phased_backproject(tg_cone_plan& p, uint64_t z0, uint64_t nz, uint64_t v0, 
   const uint64_t chunk = ((np + kChunks - 1) / kChunks + kGroup - 1) / kGroup * kGroup;
   const int n_chunks = int((np + chunk - 1) / chunk);
   const int n_phases = int(phases.size());
-  // consecutive K1 launches overlap (programmatic dependent launch)
-  const bool kPdl = std::getenv("TG_E2E_NOPDL") == nullptr;
+  // consecutive K1 launches overlap (programmatic dependent launch); not with
+  // FDK, where a K1 follows the K3 that produces its rows
+  const bool kPdl = !fdk && std::getenv("TG_E2E_NOPDL") == nullptr;
+  // FDK: one copy group per view chunk (its row segments are filtered in one
+  // K3 launch each) and whole detector rows (the filter runs along u)
+  const uint64_t G = fdk ? chunk : uint64_t(kGroup);
 
   // Per-view footprints.  K1 reads taps floor(u), floor(u)+1 (and the same in
   // v) of voxel centres only, and for w > 0 the projective image of a box of
@@ -1217,7 +1229,7 @@ void phased_backproject(tg_cone_plan& p, uint64_t z0, uint64_t nz, uint64_t v0, 
   // range per view for every phase), rows per phase, one column / row of
   // margin below and two above as in slab_rows.  At c4 this ships 35% fewer
   // bytes than the slab's row band.  A view with a corner at w <= 0 ships the
-  // caller's full band.  Copy groups of kGroup consecutive views (one 3D copy
+  // caller's full band.  Copy groups of G consecutive views (one 3D copy
   // per group and row segment, union of the group's ranges) keep the number
   // of copies small; the columns are widened to 64-byte boundaries.
   const double* vo = p.vol.origin;
@@ -1263,19 +1275,19 @@ void phased_backproject(tg_cone_plan& p, uint64_t z0, uint64_t nz, uint64_t v0, 
     if (f.ub < f.ua) f.ub = f.ua;
     return f;
   };
-  const uint64_t n_groups = (np + kGroup - 1) / kGroup;
+  const uint64_t n_groups = (np + G - 1) / G;
   // group columns: union over the group's views of the whole slab's footprint
   std::vector<int64_t> g_ua(n_groups, int64_t(nu)), g_ub(n_groups, 0);
   std::vector<int64_t> g_lo(n_groups, 0), g_hi(n_groups, 0);  // resident rows (absolute)
   for (uint64_t i = 0; i < np; ++i) {
     const Foot f = footprint(i, 0, nz - 1);
-    const uint64_t gi = i / kGroup;
+    const uint64_t gi = i / G;
     g_ua[gi] = std::min(g_ua[gi], f.ua);
     g_ub[gi] = std::max(g_ub[gi], f.ub);
   }
   for (uint64_t gi = 0; gi < n_groups; ++gi) {
-    g_ua[gi] = g_ua[gi] / 16 * 16;
-    g_ub[gi] = std::min<int64_t>(int64_t(nu), (g_ub[gi] + 15) / 16 * 16);
+    g_ua[gi] = fdk ? 0 : g_ua[gi] / 16 * 16;
+    g_ub[gi] = fdk ? int64_t(nu) : std::min<int64_t>(int64_t(nu), (g_ub[gi] + 15) / 16 * 16);
   }
 
   HostPipe hp(n_phases * n_chunks + n_phases + int(units) + 1);
@@ -1288,10 +1300,17 @@ void phased_backproject(tg_cone_plan& p, uint64_t z0, uint64_t nz, uint64_t v0, 
     TG_CUDA(cudaMemcpyAsync(h_slab + r.z * plane, d_slab + r.z * plane, r.n * plane * sizeof(float),
                             cudaMemcpyDeviceToHost, ds));
   };
+  // rows [ra, rb) of views [w0, w0 + wn) just uploaded, to be weighted and
+  // filtered in place once they land (FDK)
+  std::vector<std::pair<int64_t, int64_t>> fresh;
   auto upload = [&](uint64_t w0, uint64_t wn, int64_t ua, int64_t ub, int64_t ra, int64_t rb) {
     if (ub <= ua || rb <= ra || wn == 0) return;
+    if (fdk) fresh.push_back({ra, rb});
     cudaMemcpy3DParms cp = {};
-    cp.srcPtr = make_cudaPitchedPtr(const_cast<float*>(h_band), row_bytes, row_bytes, n_rows);
+    // host views sit h_view_pitch elements apart (the band itself, or the
+    // rows of a full sinogram)
+    cp.srcPtr = make_cudaPitchedPtr(const_cast<float*>(h_band), row_bytes, row_bytes,
+                                    h_view_pitch / nu);
     cp.dstPtr = make_cudaPitchedPtr(d_band, row_bytes, row_bytes, n_rows);
     cp.srcPos = make_cudaPos(size_t(ua) * sizeof(float), size_t(ra - int64_t(v0)), size_t(w0));
     cp.dstPos = cp.srcPos;
@@ -1305,9 +1324,9 @@ void phased_backproject(tg_cone_plan& p, uint64_t z0, uint64_t nz, uint64_t v0, 
     const bool last = ph == n_phases - 1;
     for (int c = 0; c < n_chunks; ++c) {
       const uint64_t w0 = uint64_t(c) * chunk, wn = std::min(chunk, np - w0);
-      for (uint64_t gi = w0 / kGroup; gi * kGroup < w0 + wn; ++gi) {
-        const uint64_t a = std::max<uint64_t>(gi * kGroup, w0);
-        const uint64_t b = std::min<uint64_t>((gi + 1) * kGroup, w0 + wn);
+      for (uint64_t gi = w0 / G; gi * G < w0 + wn; ++gi) {
+        const uint64_t a = std::max<uint64_t>(gi * G, w0);
+        const uint64_t b = std::min<uint64_t>((gi + 1) * G, w0 + wn);
         int64_t ra = int64_t(v0 + n_rows), rb = int64_t(v0);
         for (uint64_t i = a; i < b; ++i)
           for (const Range& r : phases[ph]) {
@@ -1332,19 +1351,28 @@ void phased_backproject(tg_cone_plan& p, uint64_t z0, uint64_t nz, uint64_t v0, 
       }
       TG_CUDA(cudaEventRecord(hp.ev[ev], hp.xs));
       TG_CUDA(cudaStreamWaitEvent(hp.cs, hp.ev[ev++], 0));
+      for (const auto& sg : fresh) {  // FDK: cosine x Parker + Ram-Lak on the new rows
+        filt::RowLayout lay;
+        lay.rows_per_view = uint64_t(sg.second - sg.first);
+        lay.view_pitch = n_rows * nu;
+        float* seg = d_band + (w0 * n_rows + uint64_t(sg.first) - v0) * nu;
+        prefilter_impl(p, seg, seg, use_parker, uint64_t(sg.first), lay.rows_per_view, w0, wn,
+                       hp.cs, lay);
+      }
+      fresh.clear();
       if (last && c == n_chunks - 1) {
         for (const Range& r : phases[ph])
           for (uint64_t q = 0; q < r.n; q += 32) {
             const Range part{r.z + q, std::min<uint64_t>(32, r.n - q)};
             backproject_impl(p, z0 + part.z, part.n, v0, n_rows, d_band, d_slab + part.z * plane,
-                             1.0f, c > 0, hp.cs, w0, wn, kPdl);
+                             scale, c > 0, hp.cs, w0, wn, kPdl);
             TG_CUDA(cudaEventRecord(hp.ev[ev], hp.cs));
             TG_CUDA(cudaStreamWaitEvent(ds, hp.ev[ev++], 0));
             download(part);
           }
       } else {
         for (const Range& r : phases[ph])
-          backproject_impl(p, z0 + r.z, r.n, v0, n_rows, d_band, d_slab + r.z * plane, 1.0f,
+          backproject_impl(p, z0 + r.z, r.n, v0, n_rows, d_band, d_slab + r.z * plane, scale,
                            c > 0, hp.cs, w0, wn, kPdl);
       }
     }

@@ -249,7 +249,7 @@ __global__ void __launch_bounds__(P / 16, (min_blocks<P, PW>())) filter_kernel(c
                                                         uint64_t n_rows, int packed,
                                                         const float* __restrict__ w,
                                                         const float2* __restrict__ tw,
-                                                        PreWeights pw) {
+                                                        PreWeights pw, RowLayout lay) {
   extern __shared__ float2 sm[];
   constexpr int PADDED = P + P / 16;
   float2* A = sm;
@@ -257,10 +257,12 @@ __global__ void __launch_bounds__(P / 16, (min_blocks<P, PW>())) filter_kernel(c
   RowIO io;
   io.ra = packed ? 2 * uint64_t(blockIdx.x) : uint64_t(blockIdx.x);
   const bool has_b = packed && io.ra + 1 < n_rows;
-  io.pa = in + io.ra * uint64_t(n);
-  io.pb = has_b ? io.pa + n : nullptr;
-  io.oa = out + io.ra * uint64_t(n);
-  io.ob = has_b ? io.oa + n : nullptr;
+  const uint64_t offa = row_offset(io.ra, n, lay);
+  const uint64_t offb = has_b ? row_offset(io.ra + 1, n, lay) : 0;
+  io.pa = in + offa;
+  io.pb = has_b ? in + offb : nullptr;
+  io.oa = out + offa;
+  io.ob = has_b ? out + offb : nullptr;
   io.n = n;
   io.pw = pw;
   io.w = w;

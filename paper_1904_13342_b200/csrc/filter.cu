@@ -207,12 +207,13 @@ void destroy(RowFilter* f) {
 // c4's band.
 constexpr int kPwRows = 8;
 __global__ void __launch_bounds__(32 * kPwRows) preweight_kernel(const float* in, float* out, int n,
-                                                                 uint64_t n_rows, PreWeights pw) {
+                                                                 uint64_t n_rows, PreWeights pw,
+                                                                 RowLayout lay) {
   const uint64_t row = uint64_t(blockIdx.x) * kPwRows + (threadIdx.x >> 5);
   if (row >= n_rows) return;
   const int lane = threadIdx.x & 31;
-  const float* src = in + row * uint64_t(n);
-  float* dst = out + row * uint64_t(n);
+  const float* src = in + row_offset(row, n, lay);
+  float* dst = out + row_offset(row, n, lay);
   const double* cw = pw.cos ? pw.cos + (pw.cos_row0 + row % pw.rows_per_view) * uint64_t(n) : nullptr;
   const double* pk = pw.parker ? pw.parker + (row / pw.rows_per_view) * uint64_t(n) : nullptr;
   auto weigh = [&](float v, int j) {
@@ -245,10 +246,12 @@ __global__ void __launch_bounds__(32 * kPwRows) preweight_kernel(const float* in
 }
 
 void apply(const RowFilter& f, const float* d_in, float* d_out, uint64_t n_rows,
-           const PreWeights* pw, cudaStream_t st) {
+           const PreWeights* pw, cudaStream_t st, RowLayout lay) {
   if (n_rows == 0) return;
   DeviceGuard dg(f.device);
   PreWeights w = pw ? *pw : PreWeights{};
+  check(lay.rows_per_view == 0 || (f.P >= 512 && f.P <= 8192),
+        "strided row layouts need a filter window in [512, 8192]");
   const bool packed = f.symmetric;
   const uint64_t blocks = packed ? (n_rows + 1) / 2 : n_rows;
   check(blocks <= 2147483647ull, "too many detector rows for one filter launch");
@@ -264,7 +267,7 @@ void apply(const RowFilter& f, const float* d_in, float* d_out, uint64_t n_rows,
     check(n_rows <= 2147483647ull, "too many detector rows for one filter launch");
     const uint64_t pw_blocks = (n_rows + kPwRows - 1) / kPwRows;
     check(pw_blocks <= 2147483647ull, "too many detector rows for one filter launch");
-    preweight_kernel<<<unsigned(pw_blocks), 32 * kPwRows, 0, st>>>(d_in, d_out, n, n_rows, w);
+    preweight_kernel<<<unsigned(pw_blocks), 32 * kPwRows, 0, st>>>(d_in, d_out, n, n_rows, w, lay);
     TG_LAUNCHED(1);
     src = d_out;
     w = PreWeights{};
@@ -272,7 +275,7 @@ void apply(const RowFilter& f, const float* d_in, float* d_out, uint64_t n_rows,
   auto launch16 = [&](auto kern, int P, size_t smem) {
     TG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     kern<<<unsigned(blocks), P / 16, smem, st>>>(src, d_out, n, n_rows, int(packed), f.d_w, f.d_tw16,
-                                                  w);
+                                                  w, lay);
   };
   const bool half = 2 * f.n <= f.P;  // the row fills at most half the window
 #define TG_LAUNCH16(PP)                                                                   \

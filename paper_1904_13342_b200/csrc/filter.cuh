@@ -41,8 +41,20 @@ int weight_grad_parts(uint64_t n_rows);
 void weight_grad(const float* d_x, const float* d_g, float* d_gk, double* d_partial,
                  uint64_t n_rows, uint64_t n, uint64_t P, bool accumulate, cudaStream_t st);
 void destroy(RowFilter* f);
+// Row r of a launch starts at (r / rows_per_view) * view_pitch +
+// (r % rows_per_view) * n elements (rows_per_view = 0: rows are contiguous) —
+// a row segment of every view of a band buffer.  Strided layouts need a
+// window P in [512, 8192] (the register FFT path).
+struct RowLayout {
+  uint64_t rows_per_view = 0;
+  uint64_t view_pitch = 0;
+};
+__host__ __device__ inline uint64_t row_offset(uint64_t r, int n, const RowLayout& L) {
+  return L.rows_per_view ? (r / L.rows_per_view) * L.view_pitch + (r % L.rows_per_view) * uint64_t(n)
+                         : r * uint64_t(n);
+}
 void apply(const RowFilter& f, const float* d_in, float* d_out, uint64_t n_rows,
-           const PreWeights* pw, cudaStream_t st);
+           const PreWeights* pw, cudaStream_t st, RowLayout lay = RowLayout{});
 
 }  // namespace filt
 }  // namespace tgb
