@@ -127,12 +127,15 @@ def test_fbp_parity(tg, O):
 
 
 @pytest.mark.parametrize("parker", [True, False])
-def test_fdk_host_row_band(tg, O, parker):
+@pytest.mark.parametrize("nu", [64, 260])
+def test_fdk_host_row_band(tg, O, parker, nu):
     """FDK from a host sinogram (tg_cone_fdk_host, the C++ drop-in's path)
     uploads and filters only the detector rows the volume projects onto:
     rows outside that band may hold anything (NaN here) and the result still
-    matches the device FDK of the clean data and the oracle"""
-    geo, og = cone_pair(tg, O, [40, 36, 24], [1.0] * 3, 64, 140, 1.0, 1.0, 60,
+    matches the device FDK of the clean data and the oracle.  nu = 64 (window
+    128) takes the view-chunk pipeline, nu = 260 (window 1024) the centre-out
+    phased one with strided row-segment filtering"""
+    geo, og = cone_pair(tg, O, [40, 36, 24], [1.0] * 3, nu, 140, 1.0, 1.0, 60,
                         220 * math.pi / 180, 300.0, 600.0)
     ph = O.shepp_logan_3d(og.vol)
     sino = O.cone_forward(og, ph)
