@@ -698,11 +698,6 @@ int default_k1_k() {
   return (e && std::atoi(e) == 16) ? 16 : 32;
 }
 
-int env_int(const char* name, int dflt) {
-  const char* e = std::getenv(name);
-  return e ? std::atoi(e) : dflt;
-}
-
 int pick_boxu(int need) {
   static const int choices[] = {48, 80, 112, 176, 240};
   for (int c : choices)
