@@ -1215,9 +1215,9 @@ void phased_backproject(tg_cone_plan& p, uint64_t z0, uint64_t nz, uint64_t v0, 
   const uint64_t chunk = ((np + kChunks - 1) / kChunks + kGroup - 1) / kGroup * kGroup;
   const int n_chunks = int((np + chunk - 1) / chunk);
   const int n_phases = int(phases.size());
-  // consecutive K1 launches overlap (programmatic dependent launch); not with
-  // FDK, where a K1 follows the K3 that produces its rows
-  const bool kPdl = !fdk && std::getenv("TG_E2E_NOPDL") == nullptr;
+  // consecutive K1 launches overlap (programmatic dependent launch); never a
+  // K1 right after the K3 that produces its rows (FDK)
+  const bool kPdl = std::getenv("TG_E2E_NOPDL") == nullptr;
   // FDK: one copy group per view chunk (its row segments are filtered in one
   // K3 launch each) and whole detector rows (the filter runs along u)
   const uint64_t G = fdk ? chunk : uint64_t(kGroup);
@@ -1351,6 +1351,7 @@ void phased_backproject(tg_cone_plan& p, uint64_t z0, uint64_t nz, uint64_t v0, 
       }
       TG_CUDA(cudaEventRecord(hp.ev[ev], hp.xs));
       TG_CUDA(cudaStreamWaitEvent(hp.cs, hp.ev[ev++], 0));
+      const bool filtered = !fresh.empty();
       for (const auto& sg : fresh) {  // FDK: cosine x Parker + Ram-Lak on the new rows
         filt::RowLayout lay;
         lay.rows_per_view = uint64_t(sg.second - sg.first);
@@ -1359,21 +1360,27 @@ void phased_backproject(tg_cone_plan& p, uint64_t z0, uint64_t nz, uint64_t v0, 
         prefilter_impl(p, seg, seg, use_parker, uint64_t(sg.first), lay.rows_per_view, w0, wn,
                        hp.cs, lay);
       }
+      // PDL only for a K1 whose stream predecessor is another K1: with FDK the
+      // chunk's first K1 follows the K3 that filtered its rows
+      bool after_k3 = fdk && filtered;
       fresh.clear();
       if (last && c == n_chunks - 1) {
         for (const Range& r : phases[ph])
           for (uint64_t q = 0; q < r.n; q += 32) {
             const Range part{r.z + q, std::min<uint64_t>(32, r.n - q)};
             backproject_impl(p, z0 + part.z, part.n, v0, n_rows, d_band, d_slab + part.z * plane,
-                             scale, c > 0, hp.cs, w0, wn, kPdl);
+                             scale, c > 0, hp.cs, w0, wn, kPdl && !after_k3);
+            after_k3 = false;
             TG_CUDA(cudaEventRecord(hp.ev[ev], hp.cs));
             TG_CUDA(cudaStreamWaitEvent(ds, hp.ev[ev++], 0));
             download(part);
           }
       } else {
-        for (const Range& r : phases[ph])
+        for (const Range& r : phases[ph]) {
           backproject_impl(p, z0 + r.z, r.n, v0, n_rows, d_band, d_slab + r.z * plane, scale,
-                           c > 0, hp.cs, w0, wn, kPdl);
+                           c > 0, hp.cs, w0, wn, kPdl && !after_k3);
+          after_k3 = false;
+        }
       }
     }
     if (!last) {
