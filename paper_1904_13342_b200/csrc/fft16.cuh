@@ -131,7 +131,12 @@ __device__ __forceinline__ float preweight(float v, const PreWeights& pw, uint64
 // true for the FDK window next_pow2(2 n)): in the first pass inputs r >= R/2
 // are zero and in the last pass outputs r >= R/2 are discarded, so the
 // compiler prunes that half of the butterfly arithmetic.
-template <int P, int R, bool INV, int SRC, int DST, bool PW = true, bool HALF = false>
+// NZR < 16 (P = 4096 only, where the first and the last pass both have radix
+// 16 and stride 256): the row occupies the first 256 * NZR samples, so only
+// NZR of each first-pass butterfly's inputs are non-zero and only NZR of each
+// last-pass butterfly's outputs are kept — the compiler drops the rest of
+// the DFT16 arithmetic (c4: 1248 samples, NZR = 5 instead of HALF's 8).
+template <int P, int R, bool INV, int SRC, int DST, bool PW = true, bool HALF = false, int NZR = 16>
 __device__ __forceinline__ void pass(const float2* __restrict__ x, float2* __restrict__ y, int Ns,
                                      const float2* __restrict__ tw, const RowIO& io) {
   constexpr int NB = P / R;          // butterflies
@@ -147,7 +152,7 @@ __device__ __forceinline__ void pass(const float2* __restrict__ x, float2* __res
       const int i = j + r * NB;
       if constexpr (SRC == SRC_GLOBAL) {
         float2 z = make_float2(0.f, 0.f);
-        if ((!HALF || r < R / 2) && i < io.n) {
+        if ((NZR < 16 ? r < NZR : (!HALF || r < R / 2)) && i < io.n) {
           if (PW) {
             z.x = preweight(io.pa[i], io.pw, io.ra, i, io.n);
             if (io.pb) z.y = preweight(io.pb[i], io.pw, io.ra + 1, i, io.n);
@@ -178,7 +183,7 @@ __device__ __forceinline__ void pass(const float2* __restrict__ x, float2* __res
       const int i = o + r * Ns;
       const float2 x_r = v[slot<R>(r)];
       if constexpr (DST == DST_GLOBAL) {
-        if ((!HALF || r < R / 2) && i < io.n) {
+        if ((NZR < 16 ? r < NZR : (!HALF || r < R / 2)) && i < io.n) {
           io.oa[i] = x_r.x * io.out_scale;
           if (io.ob) io.ob[i] = x_r.y * io.out_scale;
         }
@@ -244,7 +249,7 @@ constexpr int min_blocks() {
                             : ((512 / (P / 16)) < 1 ? 1 : ((512 / (P / 16)) > 16 ? 16 : (512 / (P / 16))));
 }
 
-template <int P, bool PW, bool HALF>
+template <int P, bool PW, bool HALF, int NZR = 16>
 __global__ void __launch_bounds__(P / 16, (min_blocks<P, PW>())) filter_kernel(const float* in, float* out, int n,
                                                         uint64_t n_rows, int packed,
                                                         const float* __restrict__ w,
@@ -269,7 +274,8 @@ __global__ void __launch_bounds__(P / 16, (min_blocks<P, PW>())) filter_kernel(c
   io.out_scale = 1.0f / float(P);
   constexpr int RL = (P == 8192) ? 2 : P / 256;  // last radix
   // forward
-  pass<P, 16, false, SRC_GLOBAL, DST_SMEM, PW, HALF>(nullptr, A, 1, tw, io);
+  static_assert(NZR == 16 || P == 4096, "pruned passes need P = 4096");
+  pass<P, 16, false, SRC_GLOBAL, DST_SMEM, PW, HALF, NZR>(nullptr, A, 1, tw, io);
   __syncthreads();
   if constexpr (P == 8192) {
     pass<P, 16, false, SRC_SMEM, DST_SMEM>(A, B, 16, tw + tw_offset<P>(16), io);
@@ -293,7 +299,7 @@ __global__ void __launch_bounds__(P / 16, (min_blocks<P, PW>())) filter_kernel(c
     __syncthreads();
     pass<P, 16, true, SRC_SMEM, DST_SMEM>(A, B, 16, tw + tw_offset<P>(16), io);
     __syncthreads();
-    pass<P, RL, true, SRC_SMEM, DST_GLOBAL, true, HALF>(B, nullptr, 256, tw + tw_offset<P>(256), io);
+    pass<P, RL, true, SRC_SMEM, DST_GLOBAL, true, HALF, NZR>(B, nullptr, 256, tw + tw_offset<P>(256), io);
   } else {
     pass<P, 16, false, SRC_SMEM, DST_SMEM>(A, B, 16, tw + tw_offset<P>(16), io);
     __syncthreads();

@@ -14,7 +14,10 @@ pytestmark = pytest.mark.gpu
 DEV = "cuda:0"
 
 
-@pytest.mark.parametrize("n,spacing", [(100, 0.7), (400, 1.0), (1248, 0.64), (365, 1.0), (5, 2.0)])
+# 1025 / 1248 / 1280: window 4096 with the pruned radix-16 first / last passes
+# (row within 5 x 256 samples); 1281: window 4096, half-window pruning only
+@pytest.mark.parametrize("n,spacing", [(100, 0.7), (400, 1.0), (1248, 0.64), (365, 1.0), (5, 2.0),
+                                       (1025, 0.5), (1280, 0.64), (1281, 0.64)])
 def test_ramlak_filter_parity(tg, O, n, spacing):
     rows = rand((7, n), 5, -1, 1)
     filt = tg.ramlak_filter(n, spacing)
@@ -39,8 +42,8 @@ def test_filter_delta_response(tg, O):
 
 
 def test_filter_nonsymmetric_weights(tg, O):
-    """test_filtering.cpp:100-127 setting: random (non-symmetric) weights take
-    the one-row-per-transform path"""
+    """test_filtering.cpp:100-127 setting: random (non-symmetric) weights —
+    symmetrised at plan creation, Re(IFFT(W X)) = IFFT(W_s X) for real rows"""
     nb, P = 10, 32
     rng = np.random.default_rng(6)
     rows = rng.uniform(-1, 1, (2, nb)).astype(np.float32)
