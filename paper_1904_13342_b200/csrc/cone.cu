@@ -975,7 +975,7 @@ void ensure_fdk_weights(tg_cone_plan& p, bool use_parker) {
 
 void prefilter_impl(tg_cone_plan& p, const float* d_in, float* d_out, bool use_parker, uint64_t v0,
                     uint64_t n_rows, uint64_t view0, uint64_t n_views, cudaStream_t st,
-                    filt::RowLayout lay = filt::RowLayout{}) {
+                    filt::RowLayout lay = filt::RowLayout{}, bool pdl = false) {
   check(n_rows >= 1 && v0 + n_rows <= p.det.n_v, "detector row band lies outside the detector");
   ensure_fdk_weights(p, use_parker);
   DeviceGuard dg(p.device);
@@ -984,7 +984,7 @@ void prefilter_impl(tg_cone_plan& p, const float* d_in, float* d_out, bool use_p
   pw.cos_row0 = v0;
   pw.rows_per_view = n_rows;
   pw.parker = use_parker ? p.d_parker + view0 * p.det.n_u : nullptr;
-  filt::apply(*p.ramlak, d_in, d_out, n_views * n_rows, &pw, st, lay);
+  filt::apply(*p.ramlak, d_in, d_out, n_views * n_rows, &pw, st, lay, pdl);
 }
 
 double fdk_scale(const tg_cone_plan& p, bool use_parker) {  // pipelines.hpp:80-81
@@ -1319,6 +1319,7 @@ void phased_backproject(tg_cone_plan& p, uint64_t z0, uint64_t nz, uint64_t v0, 
     TG_CUDA(cudaMemcpy3DAsync(&cp, hp.xs));
     shipped += uint64_t(ub - ua) * uint64_t(rb - ra) * wn * sizeof(float);
   };
+  bool k1_last = false;  // the stream's most recent kernel is a K1
   for (int ph = 0; ph < n_phases; ++ph) {
     // slices of this phase (its ranges are contiguous below / above the centre)
     const bool last = ph == n_phases - 1;
@@ -1352,13 +1353,17 @@ void phased_backproject(tg_cone_plan& p, uint64_t z0, uint64_t nz, uint64_t v0, 
       TG_CUDA(cudaEventRecord(hp.ev[ev], hp.xs));
       TG_CUDA(cudaStreamWaitEvent(hp.cs, hp.ev[ev++], 0));
       const bool filtered = !fresh.empty();
+      bool first_seg = true;
       for (const auto& sg : fresh) {  // FDK: cosine x Parker + Ram-Lak on the new rows
         filt::RowLayout lay;
         lay.rows_per_view = uint64_t(sg.second - sg.first);
         lay.view_pitch = n_rows * nu;
         float* seg = d_band + (w0 * n_rows + uint64_t(sg.first) - v0) * nu;
+        // the chunk's first pre-weights pass overlaps the previous K1's tail
+        // (that K1 reads other views' rows; the pass waits for it before exiting)
         prefilter_impl(p, seg, seg, use_parker, uint64_t(sg.first), lay.rows_per_view, w0, wn,
-                       hp.cs, lay);
+                       hp.cs, lay, kPdl && first_seg && k1_last);
+        first_seg = false;
       }
       // PDL only for a K1 whose stream predecessor is another K1: with FDK the
       // chunk's first K1 follows the K3 that filtered its rows
@@ -1371,6 +1376,7 @@ void phased_backproject(tg_cone_plan& p, uint64_t z0, uint64_t nz, uint64_t v0, 
             backproject_impl(p, z0 + part.z, part.n, v0, n_rows, d_band, d_slab + part.z * plane,
                              scale, c > 0, hp.cs, w0, wn, kPdl && !after_k3);
             after_k3 = false;
+            k1_last = true;
             TG_CUDA(cudaEventRecord(hp.ev[ev], hp.cs));
             TG_CUDA(cudaStreamWaitEvent(ds, hp.ev[ev++], 0));
             download(part);
@@ -1380,6 +1386,7 @@ void phased_backproject(tg_cone_plan& p, uint64_t z0, uint64_t nz, uint64_t v0, 
           backproject_impl(p, z0 + r.z, r.n, v0, n_rows, d_band, d_slab + r.z * plane, scale,
                            c > 0, hp.cs, w0, wn, kPdl && !after_k3);
           after_k3 = false;
+          k1_last = true;
         }
       }
     }

@@ -210,6 +210,10 @@ constexpr int kPwRows = 8;
 __global__ void __launch_bounds__(32 * kPwRows) preweight_kernel(const float* in, float* out, int n,
                                                                  uint64_t n_rows, PreWeights pw,
                                                                  RowLayout lay) {
+  // (PDL launches) the grid completes only after the stream's previous kernel
+  struct WaitPrev {
+    __device__ ~WaitPrev() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+  } wait_prev;
   const uint64_t row = uint64_t(blockIdx.x) * kPwRows + (threadIdx.x >> 5);
   if (row >= n_rows) return;
   const int lane = threadIdx.x & 31;
@@ -247,7 +251,7 @@ __global__ void __launch_bounds__(32 * kPwRows) preweight_kernel(const float* in
 }
 
 void apply(const RowFilter& f, const float* d_in, float* d_out, uint64_t n_rows,
-           const PreWeights* pw, cudaStream_t st, RowLayout lay) {
+           const PreWeights* pw, cudaStream_t st, RowLayout lay, bool pdl) {
   if (n_rows == 0) return;
   DeviceGuard dg(f.device);
   PreWeights w = pw ? *pw : PreWeights{};
@@ -268,7 +272,20 @@ void apply(const RowFilter& f, const float* d_in, float* d_out, uint64_t n_rows,
     check(n_rows <= 2147483647ull, "too many detector rows for one filter launch");
     const uint64_t pw_blocks = (n_rows + kPwRows - 1) / kPwRows;
     check(pw_blocks <= 2147483647ull, "too many detector rows for one filter launch");
-    preweight_kernel<<<unsigned(pw_blocks), 32 * kPwRows, 0, st>>>(d_in, d_out, n, n_rows, w, lay);
+    if (pdl) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(unsigned(pw_blocks));
+      cfg.blockDim = dim3(32 * kPwRows);
+      cfg.stream = st;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[0].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      TG_CUDA(cudaLaunchKernelEx(&cfg, preweight_kernel, d_in, d_out, n, n_rows, w, lay));
+    } else {
+      preweight_kernel<<<unsigned(pw_blocks), 32 * kPwRows, 0, st>>>(d_in, d_out, n, n_rows, w, lay);
+    }
     TG_LAUNCHED(1);
     src = d_out;
     w = PreWeights{};

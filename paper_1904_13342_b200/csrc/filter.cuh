@@ -53,8 +53,12 @@ __host__ __device__ inline uint64_t row_offset(uint64_t r, int n, const RowLayou
   return L.rows_per_view ? (r / L.rows_per_view) * L.view_pitch + (r % L.rows_per_view) * uint64_t(n)
                          : r * uint64_t(n);
 }
+// pdl: launch the pre-weights pass with programmatic stream serialization (it
+// may start while the stream's previous kernel drains; it waits for that
+// kernel before it exits, so its completion still implies the previous one's).
+// Only when the previous kernel neither writes these rows nor reads them.
 void apply(const RowFilter& f, const float* d_in, float* d_out, uint64_t n_rows,
-           const PreWeights* pw, cudaStream_t st, RowLayout lay = RowLayout{});
+           const PreWeights* pw, cudaStream_t st, RowLayout lay = RowLayout{}, bool pdl = false);
 
 }  // namespace filt
 }  // namespace tgb
