@@ -376,7 +376,7 @@ def main():
     for _ in range(max(2, args.warmup)):
         e2e_step()
     barrier()
-    e2e_n = max(1, min(args.steps, 5))
+    e2e_n = max(1, min(args.steps, 10))
     e2e_steps_ms = []
     t0 = time.perf_counter()
     for _ in range(e2e_n):

@@ -703,8 +703,11 @@ int default_k1_k() {
   return (e && std::atoi(e) == 16) ? 16 : 32;
 }
 
+// box widths (= shared-memory row pitch in floats); 44 before 48: a pitch of
+// 44 words spreads a warp's row-neighbour taps over more banks than 48
+// (40.53 vs 40.98 ms at c4, profiles/r1_k1_pitch.txt)
 int pick_boxu(int need) {
-  static const int choices[] = {48, 80, 112, 176, 240};
+  static const int choices[] = {44, 48, 80, 112, 176, 240};
   for (int c : choices)
     if (need <= c) return c;
   return 240;
@@ -752,6 +755,7 @@ template <int K, bool CIRC>
 void launch_bp_u(int boxU, const CUtensorMap& map, const BpArgs& a, size_t smem, cudaStream_t st,
                  bool pdl) {
   switch (boxU) {
+    case 44: return launch_bp_t<K, 44, CIRC>(map, a, smem, st, pdl);
     case 48: return launch_bp_t<K, 48, CIRC>(map, a, smem, st, pdl);
     case 80: return launch_bp_t<K, 80, CIRC>(map, a, smem, st, pdl);
     case 112: return launch_bp_t<K, 112, CIRC>(map, a, smem, st, pdl);
