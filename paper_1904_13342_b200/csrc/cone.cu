@@ -660,6 +660,31 @@ __global__ void pad_volume_t_kernel(const float* __restrict__ vol, float4* __res
 using namespace tgb;
 using namespace tgb::cone;
 
+// Host-buffer pipelines: streams and events of one call.
+struct HostPipe {
+  cudaStream_t cs = nullptr, xs = nullptr, ds = nullptr;
+  std::vector<cudaEvent_t> ev;
+  explicit HostPipe(int n_events) {
+    TG_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    TG_CUDA(cudaStreamCreateWithFlags(&xs, cudaStreamNonBlocking));
+    TG_CUDA(cudaStreamCreateWithFlags(&ds, cudaStreamNonBlocking));
+    grow(n_events);
+  }
+  void grow(int n_events) {
+    while (int(ev.size()) < n_events) {
+      cudaEvent_t e;
+      TG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      ev.push_back(e);
+    }
+  }
+  ~HostPipe() {
+    for (auto& e : ev) cudaEventDestroy(e);
+    cudaStreamDestroy(cs);
+    cudaStreamDestroy(xs);
+    cudaStreamDestroy(ds);
+  }
+};
+
 struct tg_cone_plan {
   int device = 0;
   uint64_t id = 0;
@@ -690,8 +715,18 @@ struct tg_cone_plan {
   float* d_stage_out = nullptr;
   size_t stage_out_elems = 0;
   uint64_t last_h2d_bytes = 0;  // bytes the last host-buffer call uploaded
+  std::unique_ptr<HostPipe> pipe;  // host-buffer pipeline streams / events (reused)
   std::mutex mu;
 };
+
+// The plan keeps one pipeline's streams and events across host-buffer calls
+// instead of creating and destroying ~40 CUDA objects per call.  Calls on one
+// plan are not concurrent (they also share the plan's staging buffers).
+HostPipe& plan_pipe(tg_cone_plan& p, int n_events) {
+  if (!p.pipe) p.pipe.reset(new HostPipe(n_events));
+  p.pipe->grow(n_events);
+  return *p.pipe;
+}
 
 namespace {
 
@@ -997,21 +1032,7 @@ double fdk_scale(const tg_cone_plan& p, bool use_parker) {  // pipelines.hpp:80-
 
 // Host-buffer pipelines: views in chunks, H2D on a copy stream overlapped with
 // the kernels of the previous chunk.  Staging buffers are per call.
-struct HostPipe {
-  cudaStream_t cs = nullptr, xs = nullptr;
-  std::vector<cudaEvent_t> ev;
-  explicit HostPipe(int n_events) {
-    TG_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
-    TG_CUDA(cudaStreamCreateWithFlags(&xs, cudaStreamNonBlocking));
-    ev.resize(n_events);
-    for (auto& e : ev) TG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-  }
-  ~HostPipe() {
-    for (auto& e : ev) cudaEventDestroy(e);
-    cudaStreamDestroy(cs);
-    cudaStreamDestroy(xs);
-  }
-};
+
 
 float* ensure_buffer(float*& buf, size_t& have, size_t need) {
   if (have < need) {
@@ -1087,7 +1108,7 @@ void host_backproject(tg_cone_plan& p, uint64_t z0, uint64_t nz, uint64_t v0, ui
   const int n_head = split ? n_chunks - 2 : n_chunks;
   const uint64_t pz = split ? std::max<uint64_t>(32, (nz / 8 + 31) / 32 * 32) : nz;
   const int n_parts = int((nz + pz - 1) / pz);
-  HostPipe hp(n_chunks + n_parts);
+  HostPipe& hp = plan_pipe(p, n_chunks + n_parts);
   const float scale = fdk ? float(fdk_scale(p, use_parker)) : 1.0f;
   p.last_h2d_bytes = np * per_view * sizeof(float);
   for (int c = 0; c < n_chunks; ++c) {
@@ -1294,9 +1315,8 @@ void phased_backproject(tg_cone_plan& p, uint64_t z0, uint64_t nz, uint64_t v0, 
     g_ub[gi] = fdk ? int64_t(nu) : std::min<int64_t>(int64_t(nu), (g_ub[gi] + 15) / 16 * 16);
   }
 
-  HostPipe hp(n_phases * n_chunks + n_phases + int(units) + 1);
-  cudaStream_t ds;  // downloads: concurrent with the uploads on xs
-  TG_CUDA(cudaStreamCreateWithFlags(&ds, cudaStreamNonBlocking));
+  HostPipe& hp = plan_pipe(p, n_phases * n_chunks + n_phases + int(units) + 1);
+  cudaStream_t ds = hp.ds;  // downloads: concurrent with the uploads on xs
   int ev = 0;
   uint64_t shipped = 0;
   const uint64_t row_bytes = nu * sizeof(float);
@@ -1403,7 +1423,6 @@ void phased_backproject(tg_cone_plan& p, uint64_t z0, uint64_t nz, uint64_t v0, 
   p.last_h2d_bytes = shipped;
   TG_CUDA(cudaStreamSynchronize(ds));
   TG_CUDA(cudaStreamSynchronize(hp.cs));
-  cudaStreamDestroy(ds);
 }
 
 }  // namespace
@@ -1559,7 +1578,7 @@ tg_status tg_cone_forward_host(tg_cone_plan* p, const float* h_vol, float* h_sin
     float *d_vol = nullptr, *d_sino = nullptr;
     TG_CUDA(cudaMalloc(&d_vol, nvox * sizeof(float)));
     TG_CUDA(cudaMalloc(&d_sino, p->n_proj * per_view * sizeof(float)));
-    HostPipe hp(1);
+    HostPipe& hp = plan_pipe(*p, 1);
     TG_CUDA(cudaMemcpyAsync(d_vol, h_vol, nvox * sizeof(float), cudaMemcpyHostToDevice, hp.cs));
     // views in chunks so the D2H of chunk c overlaps the projection of c+1
     const uint64_t chunk = std::max<uint64_t>(1, (p->n_proj + 7) / 8);
