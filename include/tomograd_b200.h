@@ -185,7 +185,11 @@ tg_status tg_cone_backproject_host(tg_cone_plan* plan, const float* h_sino, floa
 tg_status tg_cone_fdk_host(tg_cone_plan* plan, const float* h_sino, float* h_vol, int use_parker);
 /* host-buffer z-slab back-projection (fdk = 0) or FDK (fdk = 1) of slab
  * [z0, z0+nz) from its detector row band h_band [n_proj][n_rows][n_u]
- * (raw projections when fdk = 1) into h_slab [nz][ny][nx] */
+ * (raw projections when fdk = 1) into h_slab [nz][ny][nx].  Back-projection
+ * copies only each view's detector footprint (pixels no voxel of the slab
+ * interpolates are never read); FDK copies whole rows of the footprint's row
+ * range (the filter runs along u).  Uploads run centre-out in z so finished
+ * slices download while later rows upload. */
 tg_status tg_cone_backproject_slab_host(tg_cone_plan* plan, uint64_t z0, uint64_t nz, uint64_t v0,
                                         uint64_t n_rows, const float* h_band, float* h_slab,
                                         int fdk, int use_parker);
