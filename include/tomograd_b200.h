@@ -336,6 +336,10 @@ tg_status tg_l2_grad(const float* d_a, const float* d_b, float* d_ga, float* d_g
 tg_status tg_tv_grad(const float* d_x, float* d_gx, uint64_t nx, uint64_t ny, uint64_t nz,
                      double gs, double* d_tv, void* stream);
 
+/* graph.hpp:389-393 check_grad_finite: *d_count += number of NaN entries of
+ * d_x[0..n) (exact integer count; +-inf are not NaN, as std::isnan) */
+tg_status tg_nan_count(const float* d_x, uint64_t n, uint64_t* d_count, void* stream);
+
 /* pipelines.hpp:202-259 (experiment_learn_filter's loop), device resident on
  * a parallel / fan plan: frequency weights K (d_k: P floats; in: the initial
  * weights, out: the learned ones) descend on |pi/n BP(fourier_filter(p, K)) -
@@ -371,6 +375,20 @@ tg_status tg_rasterize_ellipses(const tg_volume_spec* vol, const double* specs, 
 /* phantom.hpp:107-128 tables scaled by fov_half_extent(vol) */
 tg_status tg_head_phantom_ellipsoids(const tg_volume_spec* vol, double* out80);
 tg_status tg_head_phantom_ellipses(const tg_volume_spec* vol, double* out60);
+
+/* ---- diagnostics ---------------------------------------------------------- */
+
+/* projector.hpp:83-107,117,138: the per-ray sample count n = ceil((t1-t0)/step)
+ * the forward projector marches (0 = the ray misses the volume), from the
+ * device's own FP64 ray setup + clip (the code K2 / K5 / K7 run).
+ * Cone: d_counts [n_views][n_v][n_u]; planar: [n_proj][n_bins]. */
+tg_status tg_cone_ray_samples(tg_cone_plan* plan, uint64_t view0, uint64_t n_views,
+                              uint64_t* d_counts, void* stream);
+tg_status tg_planar_ray_samples(tg_planar_plan* plan, uint64_t* d_counts, void* stream);
+/* plan knobs for experiments and tests (outputs are bitwise unchanged):
+ * "k2_tu" = 32 | 64 (K2 CTA width / detector band height 8 | 4 rows),
+ * "k2_dual" = 0 | 1 (keep the y-fastest quad volume for x-dominant rays) */
+tg_status tg_cone_plan_set_knob(tg_cone_plan* plan, const char* name, int64_t value);
 
 /* ---- instrumentation ---------------------------------------------------- */
 

@@ -26,6 +26,7 @@ from .graph import (BackProject, FourierFilter, ForwardProject, Graph, OpKind,  
 from .pipelines import (FilterKind, fbp_reconstruct, fdk_prefilter, fdk_reconstruct,  # noqa: F401
                         fdk_scale, make_filter)
 from .projector import (back_project, cone_backproject_slab, cone_forward_views,  # noqa: F401
+                        ray_sample_counts, set_cone_knob,
                         cone_slab_rows, forward_project)
 
 

@@ -135,6 +135,10 @@ SIGNATURES = {
                                        c_dblp, c_dblp, c_vp, c_vp]),
     "tg_planar_learn_filter_host": (c_int, [c_vp, c_vp, c_vp, c_vp, c_u64, c_dblp, c_dblp, c_dbl,
                                             c_u64, c_dblp, c_dblp, c_vp]),
+    "tg_nan_count": (c_int, [c_vp, c_u64, c_vp, c_vp]),
+    "tg_cone_ray_samples": (c_int, [c_vp, c_u64, c_u64, c_vp, c_vp]),
+    "tg_cone_plan_set_knob": (c_int, [c_vp, C.c_char_p, C.c_int64]),
+    "tg_planar_ray_samples": (c_int, [c_vp, c_vp, c_vp]),
     "tg_kernel_launch_count": (c_u64, []),
     "tg_set_timing": (None, [c_int]),
     "tg_last_kernel_ms": (c_dbl, []),

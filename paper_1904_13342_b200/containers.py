@@ -65,6 +65,10 @@ class Sinogram:
         self.detector1d = detector1d or Detector1D()
         self.detector2d = detector2d or Detector2D()
         self.cone = bool(cone)
+        if data is not None:
+            want = ((self.n_projections, int(self.detector2d.n_v), int(self.detector2d.n_u))
+                    if self.cone else (self.n_projections, int(self.detector1d.n_bins)))
+            check(tuple(data.shape) == want, "sinogram data does not match its detector")
         self.data = data
 
     @staticmethod

@@ -1,6 +1,8 @@
 // cone.cu — cone-beam plan, K1 back-projection, K2 forward projection and
 // the host-buffer pipelines.  Reference: projector.hpp:264-313 (operators),
 // pipelines.hpp:73-84 (FDK composition), geometry.hpp:126-178 (plan data).
+#include <mutex>
+#include <string>
 #include <algorithm>
 #include <memory>
 #include <cmath>
@@ -495,6 +497,33 @@ __device__ __forceinline__ bool clip_ray3(const FpArgs& a, const double o[3], co
   return t1 > t0;
 }
 
+// projector.hpp:264-281 ray setup for detector pixel (iu, iv) of view `view`
+// (d = M^-1 (iu, iv, 1), then (1/|d|) d) and its clip, in IEEE FP64 without
+// contraction.  Shared by K2 and the sample-count diagnostic, so the count
+// the test compares is the one the projector marches.
+__device__ __forceinline__ bool cone_ray(const FpArgs& a, int iu, int iv, int view, double o[3],
+                                         double d[3], double& t0, double& t1) {
+  const double* g = a.geo + 12 * view;
+  o[0] = g[0];
+  o[1] = g[1];
+  o[2] = g[2];
+  const double* M = g + 3;
+  const double X = double(iu), Y = double(iv);
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+    d[r] = DADD(DADD(DMUL(M[3 * r], X), DMUL(M[3 * r + 1], Y)), DMUL(M[3 * r + 2], 1.0));
+  const double nn = DADD(DADD(DMUL(d[0], d[0]), DMUL(d[1], d[1])), DMUL(d[2], d[2]));
+  const double s = DDIV(1.0, __dsqrt_rn(nn));
+#pragma unroll
+  for (int r = 0; r < 3; ++r) d[r] = DMUL(s, d[r]);
+  return clip_ray3(a, o, d, t0, t1);
+}
+
+// projector.hpp:117,138: n = ceil((t1 - t0) / step)
+__device__ __forceinline__ long long ray_sample_count(double span, double step) {
+  return (long long)ceil(DDIV(span, step));
+}
+
 __device__ __forceinline__ float lerpf(float a, float b, float w) { return fmaf(w, b - a, a); }
 
 // Grid: x = 32-pixel u tiles, y = views, z = 8-row v bands (slowest).  A band
@@ -516,28 +545,14 @@ __global__ void __launch_bounds__(256, TU == 32 ? 5 : 4) cone_fp_kernel(const Fp
   const int iv = blockIdx.z * (256 / TU) + (w / WPR) * 4 + (lane >> 3);
   const int vl = blockIdx.y;
   if (iu >= a.nu || iv >= a.nv) return;
-  const double* g = a.geo + 12 * (a.view0 + vl);
-  const double o[3] = {g[0], g[1], g[2]};
-  const double* M = g + 3;
-  // projector.hpp:275-277: d = M^-1 (iu, iv, 1), then (1/|d|) d
-  const double X = double(iu), Y = double(iv);
-  double d[3];
-#pragma unroll
-  for (int r = 0; r < 3; ++r)
-    d[r] = DADD(DADD(DMUL(M[3 * r], X), DMUL(M[3 * r + 1], Y)), DMUL(M[3 * r + 2], 1.0));
-  const double nn = DADD(DADD(DMUL(d[0], d[0]), DMUL(d[1], d[1])), DMUL(d[2], d[2]));
-  const double s = DDIV(1.0, __dsqrt_rn(nn));
-#pragma unroll
-  for (int r = 0; r < 3; ++r) d[r] = DMUL(s, d[r]);
-
+  double o[3], d[3], t0, t1;
   float* out = a.out + ((long long)vl * a.nv + iv) * a.nu + iu;
-  double t0, t1;
-  if (!clip_ray3(a, o, d, t0, t1)) {
+  if (!cone_ray(a, iu, iv, a.view0 + vl, o, d, t0, t1)) {
     *out = 0.0f;
     return;
   }
   const double span = DADD(t1, -t0);
-  const long long n = (long long)ceil(DDIV(span, a.step));
+  const long long n = ray_sample_count(span, a.step);
   const double dt = DDIV(span, double(n));
 
   // Sample k sits at t0 + (k + 1/2) dt; march in index space (fp32) from
@@ -593,6 +608,21 @@ __global__ void __launch_bounds__(256, TU == 32 ? 5 : 4) cone_fp_kernel(const Fp
     total += double(sum);
   }
   *out = float(total * dt);
+}
+
+// Diagnostic: the per-ray sample count K2 marches (0 = missed ray), same
+// ray setup and clip as cone_fp_kernel.  out [n_views][nv][nu].
+__global__ void __launch_bounds__(256) cone_ray_samples_kernel(const FpArgs a,
+                                                               unsigned long long* out) {
+  const int iu = blockIdx.x * 32 + (threadIdx.x & 31);
+  const int iv = blockIdx.z * 8 + (threadIdx.x >> 5);
+  const int vl = blockIdx.y;
+  if (iu >= a.nu || iv >= a.nv) return;
+  double o[3], d[3], t0, t1;
+  unsigned long long n = 0;
+  if (cone_ray(a, iu, iv, a.view0 + vl, o, d, t0, t1))
+    n = (unsigned long long)ray_sample_count(DADD(t1, -t0), a.step);
+  out[((long long)vl * a.nv + iv) * a.nu + iu] = n;
 }
 
 // builds the zero-bordered quad volume K2 gathers from (one pass over V)
@@ -706,6 +736,8 @@ struct tg_cone_plan {
   // scratch
   float4* d_vpad = nullptr;  // K2 quad volume (zero border 2)
   bool k2_dual = true;       // y-fastest copy present (memory permitting)
+  bool k2_dual_allowed = true;  // knob "k2_dual"
+  bool k2_dual_denied = false;  // the copy did not fit at the last allocation
   int k2_tu = 32;            // K2 CTA width in u (band height 256 / k2_tu rows)
   size_t vpad_elems = 0;
   float* d_pitched = nullptr;  // band copy with a 16-byte row pitch when n_u % 4 != 0
@@ -716,12 +748,18 @@ struct tg_cone_plan {
   size_t stage_out_elems = 0;
   uint64_t last_h2d_bytes = 0;  // bytes the last host-buffer call uploaded
   std::unique_ptr<HostPipe> pipe;  // host-buffer pipeline streams / events (reused)
-  std::mutex mu;
+  // Serialises every call on the plan: device-stream calls hold it while they
+  // enqueue (the plan-owned scratch below is additionally ordered across
+  // streams by ScratchOrder events), host-buffer calls for their whole
+  // duration (they share the staging buffers and pipeline streams).
+  std::recursive_mutex mu;
+  ScratchOrder vpad_order, pitched_order;
 };
 
 // The plan keeps one pipeline's streams and events across host-buffer calls
-// instead of creating and destroying ~40 CUDA objects per call.  Calls on one
-// plan are not concurrent (they also share the plan's staging buffers).
+// instead of creating and destroying ~40 CUDA objects per call.  Host-buffer
+// calls hold the plan's mutex for their whole duration (they share these and
+// the staging buffers), so concurrent calls on one plan serialise.
 HostPipe& plan_pipe(tg_cone_plan& p, int n_events) {
   if (!p.pipe) p.pipe.reset(new HostPipe(n_events));
   p.pipe->grow(n_events);
@@ -854,16 +892,21 @@ void backproject_impl(tg_cone_plan& p, uint64_t z0, uint64_t nz, uint64_t v0, ui
   check(z0 + nz <= p.vol.shape[2] && nz >= 1, "slab lies outside the volume");
   check(n_rows >= 1 && v0 + n_rows <= p.det.n_v, "detector row band lies outside the detector");
   DeviceGuard dg(p.device);
+  std::lock_guard<std::recursive_mutex> lk(p.mu);
   const uint64_t nu = p.det.n_u;
   // TMA needs 16-byte aligned rows: re-pitch the band when n_u % 4 != 0
   const float* src = d_band;
   uint64_t pitch = nu;
-  if ((nu % 4) != 0 || (reinterpret_cast<uintptr_t>(d_band) % 16) != 0) {
+  const bool repitch = (nu % 4) != 0 || (reinterpret_cast<uintptr_t>(d_band) % 16) != 0;
+  if (repitch) {
     pitch = (nu + 3) / 4 * 4;
     const size_t need = size_t(pitch) * n_rows * p.n_proj;
-    std::lock_guard<std::mutex> lk(p.mu);
+    p.pitched_order.enter(st);
     if (p.pitched_elems < need) {
-      if (p.d_pitched) TG_CUDA(cudaFree(p.d_pitched));
+      if (p.d_pitched) {
+        TG_CUDA(cudaStreamSynchronize(st));  // the buffer's last reader finished (enter above)
+        TG_CUDA(cudaFree(p.d_pitched));
+      }
       TG_CUDA(cudaMalloc(&p.d_pitched, need * sizeof(float)));
       p.pitched_elems = need;
     }
@@ -915,41 +958,42 @@ void backproject_impl(tg_cone_plan& p, uint64_t z0, uint64_t nz, uint64_t v0, ui
     c0 += cn;
   }
   timer.stop();
+  if (repitch) p.pitched_order.leave(st);
 }
 
-void ensure_vpad(tg_cone_plan& p) {
+void ensure_vpad(tg_cone_plan& p, cudaStream_t st) {
   // x-fastest and y-fastest quad volumes back to back (8.8x the volume); when
   // that does not fit next to the caller's data (volumes beyond ~1200^3 on a
   // 180 GB B200) fall back to the x-fastest copy alone (4.4x)
   const size_t one = size_t(p.vol.shape[0] + 4) * (p.vol.shape[1] + 4) * (p.vol.shape[2] + 4);
-  if (p.vpad_elems >= one * (p.k2_dual ? 2 : 1)) return;
-  if (p.d_vpad) TG_CUDA(cudaFree(p.d_vpad));
+  const bool want = p.k2_dual_allowed;
+  if (p.d_vpad) {
+    if (p.vpad_elems >= 2 * one) {
+      p.k2_dual = want;
+      return;
+    }
+    if (p.vpad_elems >= one && (!want || p.k2_dual_denied)) {
+      p.k2_dual = false;
+      return;
+    }
+    TG_CUDA(cudaStreamSynchronize(st));  // the buffer's last reader finished (enter above)
+    TG_CUDA(cudaFree(p.d_vpad));
+  }
   p.d_vpad = nullptr;
   p.vpad_elems = 0;
   size_t free_b = 0, total_b = 0;
   TG_CUDA(cudaMemGetInfo(&free_b, &total_b));
-  p.k2_dual = 2 * one * sizeof(float4) + total_b / 20 <= free_b;
+  const bool fits = 2 * one * sizeof(float4) + total_b / 20 <= free_b;
+  p.k2_dual = want && fits;
+  p.k2_dual_denied = want && !fits;
   const size_t need = one * (p.k2_dual ? 2 : 1);
   TG_CUDA(cudaMalloc(&p.d_vpad, need * sizeof(float4)));
   p.vpad_elems = need;
 }
 
-void forward_impl(tg_cone_plan& p, uint64_t view0, uint64_t nviews, const float* d_vol,
-                  float* d_out, cudaStream_t st, bool pad = true) {
-  check(view0 + nviews <= p.n_proj && nviews >= 1, "view range lies outside the geometry");
-  DeviceGuard dg(p.device);
-  std::lock_guard<std::mutex> lk(p.mu);
-  ensure_vpad(p);
+FpArgs fp_args(const tg_cone_plan& p) {
+  FpArgs a{};
   const int nx = int(p.vol.shape[0]), ny = int(p.vol.shape[1]), nz = int(p.vol.shape[2]);
-  if (pad) {
-    pad_volume_kernel<<<148 * 8, 256, 0, st>>>(d_vol, p.d_vpad, nx, ny, nz);
-    if (p.k2_dual) {
-      pad_volume_t_kernel<<<148 * 8, 256, 0, st>>>(d_vol, p.d_vpad + p.vpad_elems / 2, nx, ny, nz);
-      TG_LAUNCHED(1);
-    }
-    TG_LAUNCHED(1);
-  }
-  FpArgs a;
   a.nu = int(p.det.n_u);
   a.nv = int(p.det.n_v);
   a.nx = nx;
@@ -970,6 +1014,26 @@ void forward_impl(tg_cone_plan& p, uint64_t view0, uint64_t nviews, const float*
   a.vqT = p.k2_dual ? p.d_vpad + p.vpad_elems / 2 : nullptr;
   a.nxp = nx + 4;
   a.nyp = ny + 4;
+  return a;
+}
+
+void forward_impl(tg_cone_plan& p, uint64_t view0, uint64_t nviews, const float* d_vol,
+                  float* d_out, cudaStream_t st, bool pad = true) {
+  check(view0 + nviews <= p.n_proj && nviews >= 1, "view range lies outside the geometry");
+  DeviceGuard dg(p.device);
+  std::lock_guard<std::recursive_mutex> lk(p.mu);
+  p.vpad_order.enter(st);
+  ensure_vpad(p, st);
+  const int nx = int(p.vol.shape[0]), ny = int(p.vol.shape[1]), nz = int(p.vol.shape[2]);
+  if (pad) {
+    pad_volume_kernel<<<148 * 8, 256, 0, st>>>(d_vol, p.d_vpad, nx, ny, nz);
+    if (p.k2_dual) {
+      pad_volume_t_kernel<<<148 * 8, 256, 0, st>>>(d_vol, p.d_vpad + p.vpad_elems / 2, nx, ny, nz);
+      TG_LAUNCHED(1);
+    }
+    TG_LAUNCHED(1);
+  }
+  FpArgs a = fp_args(p);
   KernelTimer timer;
   timer.start(st);
   // one launch per <= 65535 views (grid z limit)
@@ -986,12 +1050,13 @@ void forward_impl(tg_cone_plan& p, uint64_t view0, uint64_t nviews, const float*
     TG_LAUNCHED(1);
   }
   timer.stop();
+  p.vpad_order.leave(st);
 }
 
 void ensure_fdk_weights(tg_cone_plan& p, bool use_parker) {
   tg_cone_geometry g{p.vol, p.det, p.n_proj, p.range, p.sid, p.sdd, p.mats.data(), p.sources.data(),
                      p.invs.data(), p.angles.data()};
-  std::lock_guard<std::mutex> lk(p.mu);
+  std::lock_guard<std::recursive_mutex> lk(p.mu);
   if (!p.d_cos) {
     std::vector<double> cw(p.det.n_u * p.det.n_v);
     cosine_weights_cone(g, cw.data());
@@ -1062,6 +1127,8 @@ void host_backproject(tg_cone_plan& p, uint64_t z0, uint64_t nz, uint64_t v0, ui
   check(z0 + nz <= p.vol.shape[2] && nz >= 1, "slab lies outside the volume");
   check(n_rows >= 1 && v0 + n_rows <= p.det.n_v, "detector row band lies outside the detector");
   DeviceGuard dg(p.device);
+  // the whole call: staging buffers and pipeline streams are the plan's
+  std::lock_guard<std::recursive_mutex> call_lock(p.mu);
   const uint64_t np = p.n_proj, per_view = p.det.n_u * n_rows;
   const uint64_t nvox = p.vol.shape[0] * p.vol.shape[1] * nz;
   if (fdk) ensure_fdk_weights(p, use_parker);
@@ -1083,12 +1150,8 @@ void host_backproject(tg_cone_plan& p, uint64_t z0, uint64_t nz, uint64_t v0, ui
     starts.push_back(np);
   }
   const int n_chunks = int(starts.size()) - 1;
-  float *d_band, *d_slab;
-  {
-    std::lock_guard<std::mutex> lk(p.mu);
-    d_band = ensure_buffer(p.d_stage_in, p.stage_in_elems, np * per_view);
-    d_slab = ensure_buffer(p.d_stage_out, p.stage_out_elems, nvox);
-  }
+  float* d_band = ensure_buffer(p.d_stage_in, p.stage_in_elems, np * per_view);
+  float* d_slab = ensure_buffer(p.d_stage_out, p.stage_out_elems, nvox);
   if (h_view_pitch == 0) h_view_pitch = per_view;
   // centre-out phased pipeline (BP: footprint uploads; FDK: whole rows, each
   // new row segment weighted and filtered as it lands — needs the register
@@ -1521,6 +1584,42 @@ tg_status tg_cone_forward_views(tg_cone_plan* p, uint64_t view0, uint64_t n_view
   return guarded([&] { forward_impl(*p, view0, n_views, d_vol, d_part, as_stream(stream)); });
 }
 
+tg_status tg_cone_ray_samples(tg_cone_plan* p, uint64_t view0, uint64_t n_views,
+                              uint64_t* d_counts, void* stream) {
+  return guarded([&] {
+    check(p != nullptr, "null plan");
+    check(view0 + n_views <= p->n_proj && n_views >= 1, "view range lies outside the geometry");
+    DeviceGuard dg(p->device);
+    FpArgs a = fp_args(*p);
+    const cudaStream_t st = as_stream(stream);
+    for (uint64_t c0 = 0; c0 < n_views; c0 += 65535) {
+      const uint64_t cn = std::min<uint64_t>(65535, n_views - c0);
+      a.view0 = int(view0 + c0);
+      dim3 grid((a.nu + 31) / 32, unsigned(cn), (a.nv + 7) / 8);
+      cone_ray_samples_kernel<<<grid, 256, 0, st>>>(
+          a, reinterpret_cast<unsigned long long*>(d_counts) + c0 * p->det.n_u * p->det.n_v);
+      TG_LAUNCHED(1);
+    }
+  });
+}
+
+tg_status tg_cone_plan_set_knob(tg_cone_plan* p, const char* name, int64_t value) {
+  return guarded([&] {
+    check(p != nullptr && name != nullptr, "null plan or knob name");
+    const std::string k(name);
+    std::lock_guard<std::recursive_mutex> lk(p->mu);
+    if (k == "k2_tu") {
+      check(value == 32 || value == 64, "k2_tu must be 32 or 64");
+      p->k2_tu = int(value);
+    } else if (k == "k2_dual") {
+      // 0: gather every ray from the x-fastest quad volume (bitwise identical)
+      p->k2_dual_allowed = value != 0;
+    } else {
+      check(false, "unknown knob");
+    }
+  });
+}
+
 tg_status tg_cone_backproject(tg_cone_plan* p, const float* d_sino, float* d_vol, float scale,
                               int accumulate, void* stream) {
   return guarded([&] {
@@ -1573,6 +1672,7 @@ tg_status tg_cone_fdk(tg_cone_plan* p, const float* d_sino, float* d_vol, float*
 tg_status tg_cone_forward_host(tg_cone_plan* p, const float* h_vol, float* h_sino) {
   return guarded([&] {
     DeviceGuard dg(p->device);
+    std::lock_guard<std::recursive_mutex> call_lock(p->mu);  // the plan's pipeline streams
     const uint64_t nvox = p->vol.shape[0] * p->vol.shape[1] * p->vol.shape[2];
     const uint64_t per_view = p->det.n_u * p->det.n_v;
     float *d_vol = nullptr, *d_sino = nullptr;

@@ -7,6 +7,7 @@
 #include <cstdint>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "tg_internal.h"
 
@@ -55,34 +56,87 @@ void record_kernel_ms(double ms);
 
 // A __constant__ bank shared by all plans of one kernel family on one
 // device.  Uploads are stream-ordered: before a plan overwrites the bank,
-// its stream waits for the last kernel that read it.
+// its stream waits for every kernel that read the previous contents — one
+// reader event per stream that launched a reader since then (a plan may
+// launch on several streams).
 struct ConstBank {
+  struct Reader {
+    cudaStream_t stream;
+    cudaEvent_t ev;
+  };
+  static constexpr int kMaxDev = 64;
+  static constexpr size_t kMaxReaders = 32;
   std::mutex mu;
-  uint64_t owner[64] = {};
-  cudaEvent_t last[64] = {};
+  uint64_t owner[kMaxDev] = {};
+  std::vector<Reader> readers[kMaxDev];
   // Call with mu held, right before launching on `stream`.
   void acquire(int dev, uint64_t plan_id, cudaStream_t stream, const void* symbol,
                const void* d_src, size_t bytes) {
-    if (!last[dev]) TG_CUDA(cudaEventCreateWithFlags(&last[dev], cudaEventDisableTiming));
     if (owner[dev] != plan_id) {
-      TG_CUDA(cudaStreamWaitEvent(stream, last[dev], 0));
+      for (const Reader& r : readers[dev])
+        if (r.stream != stream) TG_CUDA(cudaStreamWaitEvent(stream, r.ev, 0));
       TG_CUDA(cudaMemcpyToSymbolAsync(symbol, d_src, bytes, 0, cudaMemcpyDeviceToDevice, stream));
       owner[dev] = plan_id;
     }
   }
-  // Inside a CUDA-graph capture the owner cannot change (callers capture
-  // only work whose bank upload happened before the capture), so the
-  // ordering event is not recorded there.
+  // After the reader launch.  Inside a CUDA-graph capture the owner cannot
+  // change (callers capture only work whose bank upload happened before the
+  // capture), so no ordering event is recorded there.
   void release(int dev, cudaStream_t stream) {
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
     TG_CUDA(cudaStreamIsCapturing(stream, &cs));
     if (cs == cudaStreamCaptureStatusActive) return;
-    TG_CUDA(cudaEventRecord(last[dev], stream));
+    std::vector<Reader>& rs = readers[dev];
+    for (Reader& r : rs)
+      if (r.stream == stream) {
+        TG_CUDA(cudaEventRecord(r.ev, stream));
+        return;
+      }
+    if (rs.size() >= kMaxReaders) {
+      // bound the list: the oldest readers are waited for on the host
+      for (Reader& r : rs) TG_CUDA(cudaEventSynchronize(r.ev));
+      for (Reader& r : rs) cudaEventDestroy(r.ev);
+      rs.clear();
+    }
+    Reader r{stream, nullptr};
+    TG_CUDA(cudaEventCreateWithFlags(&r.ev, cudaEventDisableTiming));
+    TG_CUDA(cudaEventRecord(r.ev, stream));
+    rs.push_back(r);
   }
   void forget(uint64_t plan_id) {
     std::lock_guard<std::mutex> lk(mu);
     for (auto& o : owner)
       if (o == plan_id) o = 0;
+  }
+};
+
+// Orders the uses of one plan-owned scratch buffer across streams: a call
+// about to overwrite it first makes its own stream wait for the last stream
+// that used it (the ConstBank pattern for device memory).  Call enter()
+// before the first launch touching the buffer and leave() after the last,
+// both with the owning plan's mutex held.  Inside a CUDA-graph capture the
+// ordering is the capture's own (nothing recorded or waited on).
+struct ScratchOrder {
+  cudaEvent_t ev = nullptr;
+  cudaStream_t last = nullptr;
+  bool used = false;
+  static bool capturing(cudaStream_t st) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    TG_CUDA(cudaStreamIsCapturing(st, &cs));
+    return cs == cudaStreamCaptureStatusActive;
+  }
+  void enter(cudaStream_t st) {
+    if (used && last != st && !capturing(st)) TG_CUDA(cudaStreamWaitEvent(st, ev, 0));
+  }
+  void leave(cudaStream_t st) {
+    if (capturing(st)) return;
+    if (!ev) TG_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    TG_CUDA(cudaEventRecord(ev, st));
+    last = st;
+    used = true;
+  }
+  ~ScratchOrder() {
+    if (ev) cudaEventDestroy(ev);
   }
 };
 

@@ -1,12 +1,13 @@
-// filter.cu — K3 row filter: shared-memory Stockham FFT (radix 4, one
-// radix-2 tail when log2 P is odd), two real rows per complex transform when
-// the weights are symmetric, fused FDK pre-weights, fused truncation.
+// filter.cu — K3 row filter: register-resident radix-16 Stockham FFT
+// (fft16.cuh), two real rows per complex transform when the weights are
+// symmetric, FDK pre-weights, fused truncation.
 //
 // The reference (filtering.hpp:95-110) zero-pads each row to P, runs a
 // complex-double FFT, multiplies by the real weights, inverse-transforms
 // and keeps the first n samples.  This kernel computes the same linear map
-// in fp32 with FP64-derived twiddles; parity tolerance is stated in
-// tests/test_gpu_filter.py.
+// in fp32 with FP64-derived twiddles; the parity tolerance is stated in
+// tests/_helpers.py (REL_RMSE / FILTER_REL_RMSE) and exercised by
+// tests/test_gpu_fdk.py and tests/test_gpu_fullsize.py.
 #include <cstdlib>
 #include <cmath>
 #include <map>

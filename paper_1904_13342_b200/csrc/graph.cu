@@ -51,6 +51,18 @@ __global__ void multiply_weights_gx_kernel(const float* __restrict__ g, const fl
     gx[i] = float(double(gx[i]) + double(g[i]) * double(__ldg(w + i % block)));
 }
 
+// *count += number of NaN entries (graph.hpp:389-393 check_grad_finite tests
+// std::isnan only: +-inf passes); integer atomics, so the count is exact
+__global__ void nan_count_kernel(const float* __restrict__ g, uint64_t n,
+                                 unsigned long long* count) {
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  unsigned c = 0;
+  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
+    c += isnan(g[i]) ? 1u : 0u;
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_down_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(count, (unsigned long long)c);
+}
+
 // partial[c][j] = sum over the rows of chunk c of g x at column j
 // (grid: x over columns, y over row chunks; coalesced along j)
 __global__ void multiply_weights_gw_partial(const float* __restrict__ g, const float* __restrict__ x,
@@ -130,6 +142,15 @@ tg_status tg_multiply_weights_grad(const float* d_g, const float* d_x, const flo
       TG_LAUNCHED(2);
       TG_CUDA(cudaFreeAsync(partial, st));
     }
+  });
+}
+
+tg_status tg_nan_count(const float* d_x, uint64_t n, uint64_t* d_count, void* stream) {
+  return guarded([&] {
+    if (n == 0) return;
+    graph::nan_count_kernel<<<graph::grid_for(n), graph::kThreads, 0, as_stream(stream)>>>(
+        d_x, n, reinterpret_cast<unsigned long long*>(d_count));
+    TG_LAUNCHED(1);
   });
 }
 

@@ -723,7 +723,6 @@ tg_status tg_planar_learn_filter(tg_planar_plan* plan, const float* d_sino, cons
     tg_detector1d det;
     uint64_t n_proj = 0;
     tg_planar_plan_shape(plan, &vol, &det, &n_proj);
-    check(n_proj <= 2048, "learn_filter: at most 2048 views (one constant-bank view table)");
     auto ok = [](tg_status s) {
       if (s != TG_OK) throw RefError(tg_last_error());
     };
@@ -788,15 +787,15 @@ tg_status tg_planar_tv_reconstruct(tg_planar_plan* plan, const float* d_sino, fl
     auto ok = [](tg_status s) {
       if (s != TG_OK) throw RefError(tg_last_error());
     };
-    // the planar pair is graph-capturable while its view table fits one
-    // constant-bank upload (K6 chunks of 2048 views)
+    // the planar pair is graph-capturable (K4/K6 build their view maps from
+    // the plan's FP64 ray table; no constant-bank upload)
     iter::tv_loop(
         [&](const float* x, float* s, cudaStream_t q) { ok(tg_planar_forward(plan, x, s, q)); },
         [&](const float* s, float* x, cudaStream_t q) {
           ok(tg_planar_backproject(plan, s, x, 1.0f, 0, q));
         },
         n_proj * det.n_bins, vol.shape[0], vol.shape[1], 1, d_sino, d_x, iterations,
-        learning_rate, tv_lambda, h_loss_history, st, n_proj <= 2048);
+        learning_rate, tv_lambda, h_loss_history, st, true);
   });
 }
 

@@ -1,22 +1,35 @@
 // planar.cu — parallel- and fan-beam 2D operators (K4-K7).
 //   K7 parallel forward  projector.hpp:171-184   K6 parallel back  projector.hpp:186-208
 //   K5 fan forward       projector.hpp:212-230   K4 fan back (1/U^2) projector.hpp:232-260
-// Ray setup, clipping and sample counts run in IEEE FP64 without contraction
-// (bit-exact hit test and n); marching, interpolation and accumulation run
-// in fp32 with FP64 chunk anchors.
+//
+// Forward (K5/K7): one ray per (view, bin), 1-8 threads per ray.  Ray setup,
+// clip and sample count run in IEEE FP64 without contraction (bit-exact hit
+// test and n, shared with the tg_planar_ray_samples diagnostic); the march
+// runs in fp32 from FP64 anchors every 64 samples and gathers one 16-byte
+// "quad" (the four bilinear taps) per trilinear cell from a zero-bordered
+// quad image, x-fastest or y-fastest so that the lanes of a warp (adjacent
+// bins) read neighbouring quads.
+//
+// Back-projection (K4/K6): CTA = 32 x 16 pixel tile, 2 pixels per thread;
+// per (tile, view) one thread builds the view's map in FP64 at the tile
+// origin (bin = N / D with N, D affine in the pixel's tile-local index; D = 1
+// for parallel beam), shifted by an integer bin base so that the fp32
+// per-pixel evaluation works with small numbers.  The views are split over
+// the CTAs of a thread-block cluster (1 x 1 x G); partial sums are reduced
+// through distributed shared memory in a fixed order (deterministic, one
+// writer per pixel, no atomics, no scratch image).
 #include <algorithm>
 #include <memory>
 #include <vector>
 
+#include <cooperative_groups.h>
+
 #include "device_common.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace tgb {
 namespace planar {
-
-constexpr int kMaxConstViews = 2048;
-// per view (FP64): parallel -> detector axis (-r.y, r.x); fan -> ray r
-__constant__ double2 c_pviews[kMaxConstViews];
-static ConstBank g_bank;
 
 #define DADD __dadd_rn
 #define DMUL __dmul_rn
@@ -30,13 +43,18 @@ struct FpArgs {
   double sid, sdd;
   int fan;
   const double* __restrict__ rays;  // n x 2
-  const float* __restrict__ ipad;   // zero-bordered image (+2 each side)
-  int nxp;
+  // zero-bordered quads (+2 each side): element (px, py) holds
+  // (V[y][x], V[y][x+1], V[y+1][x], V[y+1][x+1]) at x = px - 2, y = py - 2
+  const float4* __restrict__ q;   // x-fastest: px + py * nxp
+  const float4* __restrict__ qT;  // y-fastest: py + px * nyp
+  int nxp, nyp;
+  int segs;  // threads per ray (1, 2, 4, 8)
   float* out;
 };
 
 __device__ __forceinline__ bool clip_ray2(const FpArgs& a, const double o[2], const double d[2],
                                           double& t0, double& t1) {
+  // projector.hpp:83-101
   const double org[2] = {a.ox, a.oy}, sp[2] = {a.sx, a.sy};
   const int n[2] = {a.nx, a.ny};
   t0 = -1e300;
@@ -62,15 +80,13 @@ __device__ __forceinline__ bool clip_ray2(const FpArgs& a, const double o[2], co
   return t1 > t0;
 }
 
-__device__ __forceinline__ float lerpf(float a, float b, float w) { return fmaf(w, b - a, a); }
-
-__global__ void __launch_bounds__(256) planar_fp_kernel(const FpArgs a) {
-  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= (long long)a.n_views * a.nb) return;
-  const int i = int(idx / a.nb), j = int(idx % a.nb);
+// projector.hpp:171-184 (parallel: origin s * axis, direction r) and
+// 212-230 (fan: source -SID r, direction normalise(pixel - source)) for bin j
+// of view i, then the clip; FP64 without contraction.
+__device__ __forceinline__ bool planar_ray(const FpArgs& a, int i, int j, double o[2], double d[2],
+                                           double& t0, double& t1) {
   const double rx = a.rays[2 * i], ry = a.rays[2 * i + 1];
   const double axx = -ry, axy = rx;
-  double o[2], d[2];
   if (!a.fan) {
     const double s = DADD(a.det_origin, DMUL(double(j), a.det_spacing));
     o[0] = DMUL(s, axx);
@@ -90,101 +106,252 @@ __global__ void __launch_bounds__(256) planar_fp_kernel(const FpArgs a) {
     d[0] = DMUL(s, dx);
     d[1] = DMUL(s, dy);
   }
-  double t0, t1;
-  if (!clip_ray2(a, o, d, t0, t1)) {
-    a.out[idx] = 0.0f;
-    return;
-  }
-  const double span = DADD(t1, -t0);
-  const long long n = (long long)ceil(DDIV(span, a.step));
-  const double dt = DDIV(span, double(n));
-  const double th = t0 + 0.5 * dt;
-  const double p0x = (o[0] + th * d[0] - a.ox) / a.sx + 2.0;
-  const double p0y = (o[1] + th * d[1] - a.oy) / a.sy + 2.0;
-  const double ddx = dt * d[0] / a.sx, ddy = dt * d[1] / a.sy;
-  const float fdx = float(ddx), fdy = float(ddy);
-  double total = 0.0;
-  for (long long k0 = 0; k0 < n; k0 += 64) {
-    // integer cell + small fp32 offset keeps sample positions precise
-    const double ax = p0x + double(k0) * ddx, ay = p0y + double(k0) * ddy;
-    const double cx = floor(ax), cy = floor(ay);
-    const float bx = float(ax - cx), by = float(ay - cy);
-    const float* cell = a.ipad + (long long)cy * a.nxp + (long long)cx;
-    const int m = int(min(64LL, n - k0));
-    float sum = 0.0f;
-    for (int k = 0; k < m; ++k) {
-      const float px = fmaf(float(k), fdx, bx), py = fmaf(float(k), fdy, by);
-      const float fx = floorf(px), fy = floorf(py);
-      const float wx = px - fx, wy = py - fy;
-      const float* b = cell + (long long)int(fy) * a.nxp + int(fx);
-      sum += lerpf(lerpf(__ldg(b), __ldg(b + 1), wx), lerpf(__ldg(b + a.nxp), __ldg(b + a.nxp + 1), wx),
-                   wy);
-    }
-    total += double(sum);
-  }
-  a.out[idx] = float(total * dt);
+  return clip_ray2(a, o, d, t0, t1);
 }
 
+// projector.hpp:117: n = ceil((t1 - t0) / step)
+__device__ __forceinline__ long long ray_sample_count(double span, double step) {
+  return (long long)ceil(DDIV(span, step));
+}
+
+__device__ __forceinline__ float lerpf(float a, float b, float w) { return fmaf(w, b - a, a); }
+
+// MUFU reciprocal (<= 1 ulp)
+__device__ __forceinline__ float rcp_approx(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
+// K5 / K7.  Lane layout: a warp holds 32 / S rays (consecutive bins of a
+// view) x S segments; segment s marches the 64-sample chunks s, s + S, ...
+// of its ray and the segments are summed by a fixed shuffle tree.
+__global__ void __launch_bounds__(256) planar_fp_kernel(const FpArgs a) {
+  const int S = a.segs;
+  const int rpw = 32 / S;
+  const int lane = threadIdx.x & 31;
+  const int seg = lane / rpw;
+  const long long ray = (long long)((blockIdx.x * 256 + threadIdx.x) >> 5) * rpw + lane % rpw;
+  const long long total_rays = (long long)a.n_views * a.nb;
+  double total = 0.0, dt = 0.0;
+  bool hit = false;
+  if (ray < total_rays) {
+    const int i = int(ray / a.nb), j = int(ray % a.nb);
+    double o[2], d[2], t0, t1;
+    hit = planar_ray(a, i, j, o, d, t0, t1);
+    if (hit) {
+      const double span = DADD(t1, -t0);
+      const long long n = ray_sample_count(span, a.step);
+      dt = DDIV(span, double(n));
+      // sample k at t0 + (k + 1/2) dt (projector.hpp:109-128), in padded
+      // index coordinates
+      const double th = t0 + 0.5 * dt;
+      const double p0x = (o[0] + th * d[0] - a.ox) / a.sx + 2.0;
+      const double p0y = (o[1] + th * d[1] - a.oy) / a.sy + 2.0;
+      const double ddx = dt * d[0] / a.sx, ddy = dt * d[1] / a.sy;
+      const float fdx = float(ddx), fdy = float(ddy);
+      // rays running mostly along x: adjacent bins are displaced along y,
+      // so gather from the y-fastest quads
+      const bool xdom = fabs(d[0]) > fabs(d[1]);
+      const float4* base = xdom ? a.qT : a.q;
+      const int stx = xdom ? a.nyp : 1, sty = xdom ? 1 : a.nxp;
+      constexpr float MAGIC = 12582912.0f;  // 1.5 * 2^23: t = M + floor(p) under round-down
+      constexpr int MAGIC_BITS = 0x4B400000;
+      for (long long k0 = 64LL * seg; k0 < n; k0 += 64LL * S) {
+        const double ax = p0x + double(k0) * ddx, ay = p0y + double(k0) * ddy;
+        const double cx = floor(ax), cy = floor(ay);
+        const float bx = float(ax - cx), by = float(ay - cy);
+        const float4* cell = base + (long long)cy * sty + (long long)cx * stx;
+        const int m = int(min(64LL, n - k0));
+        float sum = 0.0f;
+        int prev = 0x7fffffff;
+        float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 4
+        for (int k = 0; k < m; ++k) {
+          const float px = fmaf(float(k), fdx, bx), py = fmaf(float(k), fdy, by);
+          const float tx = __fadd_rd(px, MAGIC), ty = __fadd_rd(py, MAGIC);
+          const float wx = px - (tx - MAGIC), wy = py - (ty - MAGIC);
+          const int off = (__float_as_int(tx) - MAGIC_BITS) * stx + (__float_as_int(ty) - MAGIC_BITS) * sty;
+          if (off != prev) {
+            q = __ldg(cell + off);
+            prev = off;
+          }
+          sum += lerpf(lerpf(q.x, q.y, wx), lerpf(q.z, q.w, wx), wy);
+        }
+        total += double(sum);
+      }
+    }
+  }
+  // segments of one ray sit rpw lanes apart: fixed tree, lane seg 0 ends
+  // with the sum over all segments
+  for (int off = rpw; off < 32; off <<= 1) total += __shfl_down_sync(0xffffffffu, total, off);
+  if (seg == 0 && ray < total_rays) a.out[ray] = hit ? float(total * dt) : 0.0f;
+}
+
+// Diagnostic: per-ray sample count of K5/K7 (0 = missed ray), same setup.
+__global__ void __launch_bounds__(256) planar_ray_samples_kernel(const FpArgs a,
+                                                                 unsigned long long* out) {
+  const long long ray = (long long)blockIdx.x * 256 + threadIdx.x;
+  if (ray >= (long long)a.n_views * a.nb) return;
+  double o[2], d[2], t0, t1;
+  unsigned long long n = 0;
+  if (planar_ray(a, int(ray / a.nb), int(ray % a.nb), o, d, t0, t1))
+    n = (unsigned long long)ray_sample_count(DADD(t1, -t0), a.step);
+  out[ray] = n;
+}
+
+// builds both quad layouts of the zero-bordered image in one pass
+__global__ void pad_quads_kernel(const float* __restrict__ img, float4* __restrict__ q,
+                                 float4* __restrict__ qT, int nx, int ny) {
+  const int nxp = nx + 4, nyp = ny + 4;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < (long long)nxp * nyp;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int px = int(i % nxp), py = int(i / nxp);
+    const int x = px - 2, y = py - 2;
+    auto at = [&](int xx, int yy) {
+      return (xx >= 0 && xx < nx && yy >= 0 && yy < ny) ? __ldg(img + (long long)yy * nx + xx) : 0.0f;
+    };
+    const float4 v = make_float4(at(x, y), at(x + 1, y), at(x, y + 1), at(x + 1, y + 1));
+    q[i] = v;
+    qT[(long long)px * nyp + py] = v;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K4 / K6
+
+constexpr int kTX = 32, kTY = 16;  // pixel tile
+constexpr int kChunk = 128;        // views whose maps sit in shared memory at once
+constexpr int kMaxCluster = 8;
+
 struct BpArgs {
-  int nx, ny, nb, n_views, view_base;
+  int nx, ny, nb, n_views;
+  int vpg;  // views per cluster rank
   double ox, oy, sx, sy;
-  double det_origin, inv_ds;
+  double det_origin, det_spacing, inv_ds;
   double sid, sdd;
-  int fan;
+  const double* __restrict__ rays;  // n x 2
   float scale;
   int accumulate;
   const float* __restrict__ sino;
   float* img;
 };
 
-// zero-padded linear interpolation along one sinogram row (projector.hpp:32-41)
-__device__ __forceinline__ double interp_row(const float* __restrict__ row, int n, double t) {
-  const double f = floor(t);
-  const int i0 = int(f);
-  const double w1 = t - f;
-  double acc = 0.0;
-  if (i0 >= 0 && i0 < n) acc += (1.0 - w1) * double(__ldg(row + i0));
-  if (i0 + 1 >= 0 && i0 + 1 < n) acc += w1 * double(__ldg(row + i0 + 1));
-  return acc;
+// tile-local map of one view: bin - base = (n0 + lx na + ly nb) / (d0 + lx da + ly db)
+struct ViewMap {
+  float n0, na, nb, d0, da, db, w;  // w = SID (fan; weight (SID / D)^2) or 0 (parallel)
+  int base;
+};
+
+// FP64 map of view i for the tile at pixel (x0, y0), mirroring
+// projector.hpp:186-208 (parallel) / 232-260 (fan) for the tile-origin pixel.
+template <bool FAN>
+__device__ ViewMap make_map(const BpArgs& a, int i, int x0, int y0) {
+  const double rx = a.rays[2 * i], ry = a.rays[2 * i + 1];
+  const double axx = -ry, axy = rx;  // detector axis: ray rotated +90 deg
+  const double X0 = a.ox + double(x0) * a.sx, Y0 = a.oy + double(y0) * a.sy;
+  // base: the bin at the tile centre, so tile-local bins stay small
+  const double Xc = X0 + 0.5 * kTX * a.sx, Yc = Y0 + 0.5 * kTY * a.sy;
+  ViewMap m;
+  if (!FAN) {
+    const double tc = (Xc * axx + Yc * axy - a.det_origin) * a.inv_ds;
+    const double base = floor(tc);
+    const double t0 = (X0 * axx + Y0 * axy - a.det_origin) * a.inv_ds - base;
+    m.n0 = float(t0);
+    m.na = float(a.sx * axx * a.inv_ds);
+    m.nb = float(a.sy * axy * a.inv_ds);
+    m.d0 = 1.0f;
+    m.da = 0.0f;
+    m.db = 0.0f;
+    m.w = 0.0f;
+    m.base = int(base);
+  } else {
+    const double qcx = Xc + a.sid * rx, qcy = Yc + a.sid * ry;
+    const double dc = qcx * rx + qcy * ry;
+    const double tc = dc > 0.0 ? (a.sdd * (qcx * axx + qcy * axy) / dc - a.det_origin) * a.inv_ds : 0.0;
+    const double base = floor(fmin(fmax(tc, -1e9), 1e9));
+    const double qx = X0 + a.sid * rx, qy = Y0 + a.sid * ry;
+    const double D0 = qx * rx + qy * ry;
+    const double M0 = qx * axx + qy * axy;
+    const double c = a.det_origin + base * a.det_spacing;
+    // bin - base = (SDD num - c depth) / (spacing depth)
+    m.n0 = float((a.sdd * M0 - c * D0) * a.inv_ds);
+    m.na = float((a.sdd * a.sx * axx - c * a.sx * rx) * a.inv_ds);
+    m.nb = float((a.sdd * a.sy * axy - c * a.sy * ry) * a.inv_ds);
+    m.d0 = float(D0);
+    m.da = float(a.sx * rx);
+    m.db = float(a.sy * ry);
+    m.w = float(a.sid);
+    m.base = int(base);
+  }
+  return m;
 }
 
-// K6 / K4: one thread per pixel, views from the constant bank.  These 2D
-// operators are launch-bound at the BASELINE sizes (c1 2.4e7, c2 9.4e7
-// updates), so the per-update geometry runs in FP64 like the reference.
+// zero-padded linear interpolation along a sinogram row (projector.hpp:32-41)
+__device__ __forceinline__ float interp_row(const float* __restrict__ row, int nb, int base, float t) {
+  const float f = floorf(t);
+  const float w = t - f;
+  const int i0 = base + int(f);
+  const float a0 = (unsigned)i0 < (unsigned)nb ? __ldg(row + i0) : 0.0f;
+  const float a1 = (unsigned)(i0 + 1) < (unsigned)nb ? __ldg(row + i0 + 1) : 0.0f;
+  return lerpf(a0, a1, w);
+}
+
+template <bool FAN>
 __global__ void __launch_bounds__(256) planar_bp_kernel(const BpArgs a) {
-  const int ix = blockIdx.x * 32 + threadIdx.x, iy = blockIdx.y * 8 + threadIdx.y;
-  if (ix >= a.nx || iy >= a.ny) return;
-  const double x = a.ox + double(ix) * a.sx;
-  const double y = a.oy + double(iy) * a.sy;
-  double acc = 0.0;
-  for (int i = 0; i < a.n_views; ++i) {
-    const double2 c = c_pviews[i];
-    const float* row = a.sino + (long long)(a.view_base + i) * a.nb;
-    if (!a.fan) {
-      const double s = x * c.x + y * c.y;
-      acc += interp_row(row, a.nb, (s - a.det_origin) * a.inv_ds);
-    } else {
-      const double qx = x + a.sid * c.x, qy = y + a.sid * c.y;
-      const double depth = qx * c.x + qy * c.y;
-      if (depth <= 0.0) continue;  // behind the source
-      const double u = a.sdd * (qx * -c.y + qy * c.x) / depth;
-      const double U = depth / a.sid;
-      acc += interp_row(row, a.nb, (u - a.det_origin) * a.inv_ds) / (U * U);
+  __shared__ ViewMap maps[kChunk];
+  __shared__ float part[kTX * kTY];
+  cg::cluster_group cluster = cg::this_cluster();
+  const int G = int(cluster.num_blocks());
+  const int rank = int(cluster.block_rank());
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int x0 = blockIdx.x * kTX, y0 = blockIdx.y * kTY;
+  const float lx = float(tx), ly0 = float(ty), ly1 = float(ty + 8);
+  const int v_begin = min(a.n_views, rank * a.vpg);
+  const int v_end = min(a.n_views, v_begin + a.vpg);
+  float acc0 = 0.0f, acc1 = 0.0f;
+  for (int c0 = v_begin; c0 < v_end; c0 += kChunk) {
+    const int cn = min(kChunk, v_end - c0);
+    __syncthreads();
+    if (threadIdx.x < cn) maps[threadIdx.x] = make_map<FAN>(a, c0 + threadIdx.x, x0, y0);
+    __syncthreads();
+    const float* row = a.sino + (long long)c0 * a.nb;
+#pragma unroll 2
+    for (int k = 0; k < cn; ++k, row += a.nb) {
+      const ViewMap m = maps[k];
+      const float n0 = fmaf(lx, m.na, m.n0);
+      const float nn0 = fmaf(ly0, m.nb, n0), nn1 = fmaf(ly1, m.nb, n0);
+      if (!FAN) {
+        acc0 += interp_row(row, a.nb, m.base, nn0);
+        acc1 += interp_row(row, a.nb, m.base, nn1);
+      } else {
+        const float d0 = fmaf(lx, m.da, m.d0);
+        const float dd0 = fmaf(ly0, m.db, d0), dd1 = fmaf(ly1, m.db, d0);
+        const float r0 = rcp_approx(dd0), r1 = rcp_approx(dd1);
+        const float s0 = m.w * r0, s1 = m.w * r1;  // 1/U = SID / depth
+        // depth <= 0: behind the source (projector.hpp:247)
+        if (dd0 > 0.0f) acc0 = fmaf(interp_row(row, a.nb, m.base, nn0 * r0), s0 * s0, acc0);
+        if (dd1 > 0.0f) acc1 = fmaf(interp_row(row, a.nb, m.base, nn1 * r1), s1 * s1, acc1);
+      }
     }
   }
-  float* o = a.img + (long long)iy * a.nx + ix;
-  const float v = float(acc) * a.scale;
-  *o = a.accumulate ? *o + v : v;
-}
-
-__global__ void pad_image_kernel(const float* __restrict__ img, float* __restrict__ ipad, int nx,
-                                 int ny) {
-  const int nxp = nx + 4, nyp = ny + 4;
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < (long long)nxp * nyp;
-       i += (long long)gridDim.x * blockDim.x) {
-    const int x = int(i % nxp) - 2, y = int(i / nxp) - 2;
-    ipad[i] = (x >= 0 && x < nx && y >= 0 && y < ny) ? __ldg(img + (long long)y * nx + x) : 0.0f;
+  // cluster reduction: rank r owns pixels p = r, r + G, ... of the tile and
+  // sums the G partials in rank order
+  part[ty * kTX + tx] = acc0;
+  part[(ty + 8) * kTX + tx] = acc1;
+  cluster.sync();
+  for (int p = threadIdx.x; p < kTX * kTY; p += 256) {
+    if (p % G != rank) continue;
+    float s = 0.0f;
+    for (int g = 0; g < G; ++g) s += cluster.map_shared_rank(part, g)[p];
+    const int ix = x0 + (p % kTX), iy = y0 + (p / kTX);
+    if (ix < a.nx && iy < a.ny) {
+      float* o = a.img + (long long)iy * a.nx + ix;
+      const float v = s * a.scale;
+      *o = a.accumulate ? *o + v : v;
+    }
   }
+  cluster.sync();  // keep this CTA's partials alive until every rank has read them
 }
 
 }  // namespace planar
@@ -202,80 +369,116 @@ struct tg_planar_plan {
   double range = 0, sid = 0, sdd = 0;
   bool fan = false;
   double* d_rays = nullptr;
-  double2* d_coef = nullptr;
-  float* d_ipad = nullptr;
+  float4* d_quads = nullptr;  // K5/K7 scratch: both quad layouts
+  ScratchOrder quads_order;
+  int n_sm = 148;
   std::mutex mu;
 };
 
 namespace {
 
-void planar_forward_impl(tg_planar_plan& p, const float* d_img, float* d_sino, cudaStream_t st) {
-  DeviceGuard dg(p.device);
-  std::lock_guard<std::mutex> lk(p.mu);
-  const int nx = int(p.vol.shape[0]), ny = int(p.vol.shape[1]);
-  if (!p.d_ipad) TG_CUDA(cudaMalloc(&p.d_ipad, size_t(nx + 4) * (ny + 4) * sizeof(float)));
-  pad_image_kernel<<<148 * 4, 256, 0, st>>>(d_img, p.d_ipad, nx, ny);
-  TG_LAUNCHED(1);
-  FpArgs a;
+FpArgs fp_args(const tg_planar_plan& p) {
+  FpArgs a{};
   a.nb = int(p.det.n_bins);
   a.n_views = int(p.n_proj);
-  a.nx = nx;
-  a.ny = ny;
+  a.nx = int(p.vol.shape[0]);
+  a.ny = int(p.vol.shape[1]);
   a.ox = p.vol.origin[0];
   a.oy = p.vol.origin[1];
   a.sx = p.vol.spacing[0];
   a.sy = p.vol.spacing[1];
-  a.step = 0.5 * ((a.sy < a.sx) ? a.sy : a.sx);
+  a.step = 0.5 * ((a.sy < a.sx) ? a.sy : a.sx);  // projector.hpp:103-107
   a.det_origin = p.det.origin;
   a.det_spacing = p.det.spacing;
   a.sid = p.sid;
   a.sdd = p.sdd;
   a.fan = p.fan;
   a.rays = p.d_rays;
-  a.ipad = p.d_ipad;
-  a.nxp = nx + 4;
+  a.nxp = a.nx + 4;
+  a.nyp = a.ny + 4;
+  return a;
+}
+
+void planar_forward_impl(tg_planar_plan& p, const float* d_img, float* d_sino, cudaStream_t st) {
+  DeviceGuard dg(p.device);
+  std::lock_guard<std::mutex> lk(p.mu);
+  FpArgs a = fp_args(p);
+  const size_t nq = size_t(a.nxp) * a.nyp;
+  if (!p.d_quads) TG_CUDA(cudaMalloc(&p.d_quads, 2 * nq * sizeof(float4)));
+  p.quads_order.enter(st);
+  pad_quads_kernel<<<p.n_sm * 4, 256, 0, st>>>(d_img, p.d_quads, p.d_quads + nq, a.nx, a.ny);
+  TG_LAUNCHED(1);
+  a.q = p.d_quads;
+  a.qT = p.d_quads + nq;
   a.out = d_sino;
-  const long long total = (long long)a.n_views * a.nb;
+  // threads per ray: enough threads for ~3 waves of 2048 per SM
+  const long long rays = (long long)a.n_views * a.nb;
+  int S = 1;
+  while (S < 8 && rays * S < 3LL * p.n_sm * 2048) S <<= 1;
+  a.segs = S;
+  const long long warps = (rays + 32 / S - 1) / (32 / S);
   KernelTimer timer;
   timer.start(st);
-  planar_fp_kernel<<<unsigned((total + 255) / 256), 256, 0, st>>>(a);
+  planar_fp_kernel<<<unsigned((warps + 7) / 8), 256, 0, st>>>(a);
   TG_LAUNCHED(1);
   timer.stop();
+  p.quads_order.leave(st);
+}
+
+template <bool FAN>
+void launch_bp(const BpArgs& a, dim3 grid, int G, cudaStream_t st) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 1;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = unsigned(G);
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  TG_CUDA(cudaLaunchKernelEx(&cfg, planar_bp_kernel<FAN>, a));
 }
 
 void planar_backproject_impl(tg_planar_plan& p, const float* d_sino, float* d_img, float scale,
                              int accumulate, cudaStream_t st) {
   DeviceGuard dg(p.device);
-  BpArgs a;
+  BpArgs a{};
   a.nx = int(p.vol.shape[0]);
   a.ny = int(p.vol.shape[1]);
   a.nb = int(p.det.n_bins);
+  a.n_views = int(p.n_proj);
   a.ox = p.vol.origin[0];
   a.oy = p.vol.origin[1];
   a.sx = p.vol.spacing[0];
   a.sy = p.vol.spacing[1];
   a.det_origin = p.det.origin;
-  a.inv_ds = 1.0 / p.det.spacing;
+  a.det_spacing = p.det.spacing;
+  a.inv_ds = 1.0 / p.det.spacing;  // projector.hpp:193
   a.sid = p.sid;
   a.sdd = p.sdd;
-  a.fan = p.fan;
+  a.rays = p.d_rays;
+  a.scale = scale;
+  a.accumulate = accumulate;
   a.sino = d_sino;
   a.img = d_img;
-  dim3 grid((a.nx + 31) / 32, (a.ny + 7) / 8);
+  const dim3 tiles((a.nx + kTX - 1) / kTX, (a.ny + kTY - 1) / kTY, 1);
+  // views split over a cluster of G CTAs per tile: enough CTAs for ~4 waves
+  // at 8 CTAs per SM, at least 8 views per CTA
+  const long long nt = (long long)tiles.x * tiles.y;
+  int G = int(std::min<long long>(kMaxCluster, (4LL * p.n_sm * 8 + nt - 1) / nt));
+  G = std::max(1, std::min(G, std::max(1, a.n_views / 8)));
+  a.vpg = (a.n_views + G - 1) / G;
   KernelTimer timer;
   timer.start(st);
-  for (uint64_t c0 = 0; c0 < p.n_proj; c0 += kMaxConstViews) {
-    const uint64_t cn = std::min<uint64_t>(kMaxConstViews, p.n_proj - c0);
-    a.n_views = int(cn);
-    a.view_base = int(c0);
-    a.scale = scale;
-    a.accumulate = c0 == 0 ? accumulate : 1;
-    std::lock_guard<std::mutex> lk(g_bank.mu);
-    g_bank.acquire(p.device, (p.id << 24) ^ c0, st, c_pviews, p.d_coef + c0, cn * sizeof(double2));
-    planar_bp_kernel<<<grid, dim3(32, 8), 0, st>>>(a);
-    TG_LAUNCHED(1);
-    g_bank.release(p.device, st);
-  }
+  const dim3 grid(tiles.x, tiles.y, unsigned(G));
+  if (p.fan)
+    launch_bp<true>(a, grid, G, st);
+  else
+    launch_bp<false>(a, grid, G, st);
+  TG_LAUNCHED(1);
   timer.stop();
 }
 
@@ -309,16 +512,10 @@ tg_status tg_planar_plan_create(const tg_planar_geometry* g, int device, tg_plan
     p->sdd = g->sdd;
     p->fan = fan;
     const uint64_t n = g->n_projections;
-    std::vector<double2> coef(n);
-    for (uint64_t i = 0; i < n; ++i) {
-      const double rx = g->rays[2 * i], ry = g->rays[2 * i + 1];
-      coef[i] = fan ? make_double2(rx, ry) : make_double2(-ry, rx);
-    }
     DeviceGuard dg(device);
+    TG_CUDA(cudaDeviceGetAttribute(&p->n_sm, cudaDevAttrMultiProcessorCount, device));
     TG_CUDA(cudaMalloc(&p->d_rays, 2 * n * sizeof(double)));
     TG_CUDA(cudaMemcpy(p->d_rays, g->rays, 2 * n * sizeof(double), cudaMemcpyHostToDevice));
-    TG_CUDA(cudaMalloc(&p->d_coef, n * sizeof(double2)));
-    TG_CUDA(cudaMemcpy(p->d_coef, coef.data(), n * sizeof(double2), cudaMemcpyHostToDevice));
     *out = p.release();
   });
 }
@@ -326,11 +523,9 @@ tg_status tg_planar_plan_create(const tg_planar_geometry* g, int device, tg_plan
 tg_status tg_planar_plan_destroy(tg_planar_plan* p) {
   return guarded([&] {
     if (!p) return;
-    g_bank.forget(p->id);
     DeviceGuard dg(p->device);
     cudaFree(p->d_rays);
-    cudaFree(p->d_coef);
-    cudaFree(p->d_ipad);
+    cudaFree(p->d_quads);
     delete p;
   });
 }
@@ -353,6 +548,18 @@ tg_status tg_planar_backproject(tg_planar_plan* p, const float* d_sino, float* d
                                 int accumulate, void* stream) {
   return guarded(
       [&] { planar_backproject_impl(*p, d_sino, d_img, scale, accumulate, as_stream(stream)); });
+}
+
+tg_status tg_planar_ray_samples(tg_planar_plan* p, uint64_t* d_counts, void* stream) {
+  return guarded([&] {
+    check(p != nullptr, "null plan");
+    DeviceGuard dg(p->device);
+    const FpArgs a = fp_args(*p);
+    const long long rays = (long long)a.n_views * a.nb;
+    planar_ray_samples_kernel<<<unsigned((rays + 255) / 256), 256, 0, as_stream(stream)>>>(
+        a, reinterpret_cast<unsigned long long*>(d_counts));
+    TG_LAUNCHED(1);
+  });
 }
 
 tg_status tg_planar_forward_host(tg_planar_plan* p, const float* h_img, float* h_sino) {

@@ -381,6 +381,17 @@ def tv_reconstruct_p2p(geo: ConeGeometry, p_part: torch.Tensor, iterations: int,
                                            float(tv_lambda), float(learning_rate), d_tv, st))
             sync_all()  # every slab in every next replica
             cur, nxt = nxt, cur
+            # stop together at the first non-finite loss (pipelines.hpp:166-170
+            # checks every iteration): this rank's two partials of iteration
+            # `it` are final after the barrier; one MIN over ranks of a flag
+            part = sums[2 * it:2 * it + 2].cpu()
+            ok = torch.tensor([1.0 if math.isfinite(float(part[0]) + float(part[1])) else 0.0],
+                              dtype=torch.float64,
+                              device="cpu" if dist.get_backend(group) == "gloo" else dev)
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=group)
+            if float(ok) < 1.0:
+                iterations = it
+                break
         # loss partials of all ranks, summed in rank order
         world_sums = [torch.empty_like(sums) for _ in range(world)]
         if dist.get_backend(group) == "gloo":

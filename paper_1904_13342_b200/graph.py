@@ -291,7 +291,7 @@ class Graph:
         tensors = [i for i in range(loss + 1)
                    if active[i] and isinstance(self._nodes[i].grad, torch.Tensor)]
         if tensors:
-            self._nan_slots = torch.zeros(len(self._nodes), dtype=torch.float64,
+            self._nan_slots = torch.zeros(len(self._nodes), dtype=torch.int64,
                                           device=self._nodes[tensors[0]].grad.device)
         try:
             for nid in range(loss, -1, -1):
@@ -300,8 +300,9 @@ class Graph:
         finally:
             slots = self._nan_slots.cpu().numpy() if tensors else None
             self._nan_slots = None
+        # the reference raises at the first NaN of its sweep (highest id first)
         for nid in sorted(tensors, reverse=True):
-            if math.isnan(slots[nid]):
+            if slots[nid] > 0:
                 raise N.Error(f"gradient of node {nid} contains NaN")
         return {nid: n.grad for nid, n in enumerate(self._nodes) if n.kind == OpKind.parameter}
 
@@ -378,16 +379,23 @@ class Graph:
         raise N.Error("node kind cannot be evaluated")
 
     def _check_grad_finite(self, nid: NodeId) -> None:
-        """graph.hpp:402-406; tensor gradients: sum (g - g)^2 is NaN iff an
-        entry is not finite, reduced on the device into this node's slot"""
+        """graph.hpp:389-393,402: tensor gradients count their NaN entries
+        (std::isnan: +-inf passes) on the device into this node's slot, read
+        back once per backward; a NaN scalar raises at once, unless a tensor
+        node swept before it (higher id) already holds a NaN — the reference
+        would have stopped there first."""
         g = self._nodes[nid].grad
         if not isinstance(g, torch.Tensor):
             if math.isnan(g):
+                if self._nan_slots is not None:
+                    slots = self._nan_slots.cpu().numpy()
+                    earlier = [i for i in range(len(slots) - 1, nid, -1) if slots[i] > 0]
+                    if earlier:
+                        nid = earlier[0]
                 raise N.Error(f"gradient of node {nid} contains NaN")
             return
         slot = self._nan_slots.data_ptr() + 8 * nid
-        N.check(N.lib().tg_l2_residual(g.data_ptr(), g.data_ptr(), None, g.numel(), slot,
-                                       stream_of(g)))
+        N.check(N.lib().tg_nan_count(g.data_ptr(), g.numel(), slot, stream_of(g)))
 
     def _add_grad(self, nid: NodeId, contrib, factor: float = 1.0) -> None:
         dst = self._nodes[nid]

@@ -216,6 +216,18 @@ def test_nan_gradient_is_reported(tg):
     assert str(e.value) == f"gradient of node {b} contains NaN"
 
 
+def test_inf_gradient_is_not_nan(tg):
+    """graph.hpp:389-393 tests std::isnan only: an overflowing (+-inf) gradient
+    passes the check, as in the reference"""
+    g = tg.Graph()
+    a = g.parameter(_t(np.array([1.0, float("inf"), 2.0])))
+    b = g.input([3])
+    loss = g.l2_loss(a, b)
+    g.forward({b: _t(np.zeros(3))})
+    grads = g.backward(loss)
+    assert torch.isinf(grads[a]).any() and not torch.isnan(grads[a]).any()
+
+
 def test_graph_requires_device_values(tg):
     g = tg.Graph()
     x = g.input([4])
