@@ -31,7 +31,7 @@ HOST_CXX = "/usr/bin/g++" if os.path.exists("/usr/bin/g++") else "g++"
 
 CU_SOURCES = ["runtime.cu", "cone.cu", "filter.cu", "planar.cu", "phantom.cu", "iterative.cu", "graph.cu"]
 CPP_SOURCES = ["host_geometry.cpp"]
-HEADERS = ["tg_internal.h", "device_common.cuh", "cone_kernels.cuh", "filter.cuh", "fft16.cuh"]
+HEADERS = ["tg_internal.h", "device_common.cuh", "cone_kernels.cuh", "cone_fp_slab.cuh", "filter.cuh", "fft16.cuh"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <memory>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <vector>
@@ -681,6 +682,40 @@ __global__ void pad_volume_t_kernel(const float* __restrict__ vol, float4* __res
   }
 }
 
+// Vt[z][x][y] (row pitch `pitch` >= ny floats) from V[z][y][x]: the y-fastest
+// copy the slab-staged K2 reads for x-dominant tiles; also a plain re-pitch
+// of V when nx is not a multiple of 4 (TMA strides are 16-byte multiples)
+__global__ void transpose_xy_kernel(const float* __restrict__ v, float* __restrict__ vt, int nx,
+                                    int ny, int pitch) {
+  __shared__ float tile[32][33];
+  const int z = blockIdx.z;
+  const int x0 = blockIdx.x * 32, y0 = blockIdx.y * 32;
+  const float* src = v + (long long)z * nx * ny;
+  float* dst = vt + (long long)z * nx * pitch;
+  for (int r = threadIdx.y; r < 32; r += 8) {
+    const int x = x0 + threadIdx.x, y = y0 + r;
+    tile[r][threadIdx.x] = (x < nx && y < ny) ? __ldg(src + (long long)y * nx + x) : 0.0f;
+  }
+  __syncthreads();
+  for (int r = threadIdx.y; r < 32; r += 8) {
+    const int y = y0 + threadIdx.x, x = x0 + r;
+    if (x < nx && y < pitch) dst[(long long)x * pitch + y] = tile[threadIdx.x][r];
+  }
+}
+
+__global__ void repitch_x_kernel(const float* __restrict__ v, float* __restrict__ vx, int nx,
+                                 int rows, int pitch) {
+  const long long total = (long long)rows * pitch;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int x = int(i % pitch);
+    const long long row = i / pitch;
+    vx[i] = x < nx ? __ldg(v + row * nx + x) : 0.0f;
+  }
+}
+
+#include "cone_fp_slab.cuh"
+
 }  // namespace cone
 }  // namespace tgb
 
@@ -740,6 +775,18 @@ struct tg_cone_plan {
   bool k2_dual_denied = false;  // the copy did not fit at the last allocation
   int k2_tu = 32;            // K2 CTA width in u (band height 256 / k2_tu rows)
   size_t vpad_elems = 0;
+  // slab-staged K2 (default; knob "k2_impl" 1) vs the quad-volume K2 (0)
+  int k2_impl = 1;
+  float* d_vt = nullptr;       // y-fastest copy Vt[z][x][y] (row pitch vt_pitch)
+  float* d_vx = nullptr;       // x-fastest re-pitched copy (only when nx % 4 != 0)
+  size_t vt_elems = 0, vx_elems = 0;
+  int vt_pitch = 0, vx_pitch = 0;
+  struct K2Box {
+    int tu = 16, wh = 40, t = 8, hz = 0, stages = 2;  // hz: multiple of 4
+    bool sized = false;
+  } k2box;
+  unsigned long long* d_k2_stats = nullptr;  // TG_K2_STATS=1: slab / fallback counters
+  ScratchOrder vt_order;
   float* d_pitched = nullptr;  // band copy with a 16-byte row pitch when n_u % 4 != 0
   size_t pitched_elems = 0;
   float* d_stage_in = nullptr;  // host-variant staging (reused across calls)
@@ -1017,11 +1064,248 @@ FpArgs fp_args(const tg_cone_plan& p) {
   return a;
 }
 
+// ---- slab-staged K2 (cone_fp_slab.cuh) ---------------------------------------
+
+int env_int(const char* name, int dflt) {
+  const char* e = std::getenv(name);
+  return (e && *e) ? std::atoi(e) : dflt;
+}
+
+// Host replica of the producer's box sizing over a sample of views: picks
+// the transverse box width WH (a template instance) and the z extent HZ so
+// that >= 99% of (tile, slab) boxes fit; the rest gather from global memory
+// (same bits).  Environment overrides for experiments: TG_K2_TU, TG_K2_WH,
+// TG_K2_T, TG_K2_HZ, TG_K2_STAGES.
+void k2_size_boxes(tg_cone_plan& p) {
+  auto& B = p.k2box;
+  B.tu = env_int("TG_K2_TU", 16);
+  B.t = env_int("TG_K2_T", 8);
+  const int TU = B.tu, TV = fps::NCONS / TU, T = B.t;
+  const int nx = int(p.vol.shape[0]), ny = int(p.vol.shape[1]), nz = int(p.vol.shape[2]);
+  const int nu = int(p.det.n_u), nv = int(p.det.n_v);
+  static const int kWH[] = {40, 72};  // = 8 (mod 32): see cone_fp_slab.cuh
+  constexpr int kMaxNeed = 260;
+  std::vector<uint64_t> hist(size_t(kMaxNeed) * kMaxNeed, 0);  // [wneed][zneed]
+  uint64_t total = 0;
+  const int n_sample = int(std::min<uint64_t>(p.n_proj, 12));
+  for (int si = 0; si < n_sample; ++si) {
+    const uint64_t view = (uint64_t(si) * p.n_proj) / uint64_t(n_sample);
+    const double* src = p.sources.data() + 3 * view;
+    const double* M = p.invs.data() + 9 * view;
+    const double o[3] = {(src[0] - p.vol.origin[0]) / p.vol.spacing[0],
+                         (src[1] - p.vol.origin[1]) / p.vol.spacing[1],
+                         (src[2] - p.vol.origin[2]) / p.vol.spacing[2]};
+    for (int v0 = 0; v0 < nv; v0 += TV)
+      for (int u0 = 0; u0 < nu; u0 += TU) {
+        double e[4][3];
+        double sx = 0, sy = 0;
+        for (int c = 0; c < 4; ++c) {
+          const int iu = (c & 1) ? std::min(u0 + TU, nu) - 1 : u0;
+          const int iv = (c & 2) ? std::min(v0 + TV, nv) - 1 : v0;
+          for (int r = 0; r < 3; ++r)
+            e[c][r] = (M[3 * r] * iu + M[3 * r + 1] * iv + M[3 * r + 2]) / p.vol.spacing[r];
+          sx += e[c][0];
+          sy += e[c][1];
+        }
+        const bool xdom = std::fabs(sx) > std::fabs(sy);
+        const int nd = xdom ? nx : ny;
+        double hA[4], hB[4], zA[4], zB[4];
+        bool ok = true;
+        for (int c = 0; c < 4; ++c) {
+          const double ed = xdom ? e[c][0] : e[c][1], eh = xdom ? e[c][1] : e[c][0];
+          const double od = xdom ? o[0] : o[1], oh = xdom ? o[1] : o[0];
+          const double len = std::sqrt(e[c][0] * e[c][0] + e[c][1] * e[c][1] + e[c][2] * e[c][2]);
+          ok = ok && std::fabs(ed) >= 0.3 * len;
+          hB[c] = eh / ed;
+          hA[c] = oh - od * hB[c];
+          zB[c] = e[c][2] / ed;
+          zA[c] = o[2] - od * zB[c];
+        }
+        if (!ok) continue;
+        for (int s0 = -3; s0 <= nd; s0 += T) {
+          // box planes [s0 - 1, s0 + T + 1] cover both march directions
+          double hmin = 1e300, hmax = -1e300, zmin = 1e300, zmax = -1e300;
+          for (int c = 0; c < 4; ++c)
+            for (int k = 0; k < 2; ++k) {
+              const double P = double(s0 - 1 + k * (T + 2));
+              const double hh = hA[c] + P * hB[c], zz = zA[c] + P * zB[c];
+              hmin = std::min(hmin, hh);
+              hmax = std::max(hmax, hh);
+              zmin = std::min(zmin, zz);
+              zmax = std::max(zmax, zz);
+            }
+          // slabs entirely outside the volume hold no samples
+          if (zmax < -2.0 || zmin > nz + 1.0) continue;
+          if (xdom ? (hmax < -2.0 || hmin > ny + 1.0) : (hmax < -2.0 || hmin > nx + 1.0)) continue;
+          const int hb = (int(std::floor(hmin)) - 1) & ~3, zb = int(std::floor(zmin)) - 1;
+          const int wn = std::min(kMaxNeed - 1, int(std::floor(hmax)) + 3 - hb);
+          const int zn = std::min(kMaxNeed - 1, int(std::floor(zmax)) + 3 - zb);
+          ++hist[size_t(wn) * kMaxNeed + zn];
+          ++total;
+        }
+      }
+  }
+  int wh = 72, hz = 256;
+  if (total) {
+    for (int cand : kWH) {
+      uint64_t fit = 0;
+      for (int wn = 0; wn <= cand; ++wn)
+        for (int zn = 0; zn < kMaxNeed; ++zn) fit += hist[size_t(wn) * kMaxNeed + zn];
+      if (fit >= uint64_t(0.999 * double(total)) || cand == 72) {
+        wh = cand;
+        break;
+      }
+    }
+    // smallest HZ with >= 99% of all slabs fitting (WH and HZ)
+    std::vector<uint64_t> zc(kMaxNeed, 0);
+    for (int wn = 0; wn <= wh; ++wn)
+      for (int zn = 0; zn < kMaxNeed; ++zn) zc[zn] += hist[size_t(wn) * kMaxNeed + zn];
+    uint64_t acc = 0;
+    hz = kMaxNeed - 1;
+    for (int zn = 0; zn < kMaxNeed; ++zn) {
+      acc += zc[zn];
+      if (acc >= uint64_t(0.998 * double(total))) {
+        hz = zn;
+        break;
+      }
+    }
+  }
+  B.wh = env_int("TG_K2_WH", wh);
+  B.hz = (std::max(4, std::min(256, env_int("TG_K2_HZ", hz))) + 3) & ~3;
+  // ring depth: two CTAs per SM (<= ~113 KB of shared memory each)
+  const size_t stage_bytes = size_t((B.wh * (B.t + 2) * B.hz + 31) & ~31) * 4;
+  const size_t fixed = sizeof(fps::RayState) + 1024;
+  int stages = int((113 * 1024 - fixed) / stage_bytes);
+  stages = std::max(2, std::min(fps::MAX_STAGES, stages));
+  B.stages = std::max(1, std::min(fps::MAX_STAGES, env_int("TG_K2_STAGES", stages)));
+  B.sized = true;
+  if (env_int("TG_K2_STATS", 0))
+    std::fprintf(stderr, "[k2] tu %d wh %d t %d hz %d stages %d (sampled slabs %llu)\n", B.tu,
+                 B.wh, B.t, B.hz, B.stages, (unsigned long long)total);
+}
+
+template <int TU, int WH>
+void launch_fp_slab_t(const CUtensorMap& mx, const CUtensorMap& my, const fps::Args& a, dim3 grid,
+                      size_t smem, cudaStream_t st) {
+  auto fn = fps::cone_fp_slab_kernel<TU, WH>;
+  TG_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  fn<<<grid, fps::NTHREADS, smem, st>>>(mx, my, a);
+}
+
+void launch_fp_slab(int tu, int wh, const CUtensorMap& mx, const CUtensorMap& my,
+                    const fps::Args& a, dim3 grid, size_t smem, cudaStream_t st) {
+#define TG_K2_CASE(TU_, WH_)                                  \
+  if (tu == TU_ && wh == WH_) {                               \
+    launch_fp_slab_t<TU_, WH_>(mx, my, a, grid, smem, st);    \
+    return;                                                   \
+  }
+  TG_K2_CASE(16, 40)
+  TG_K2_CASE(16, 72)
+  TG_K2_CASE(32, 40)
+  TG_K2_CASE(32, 72)
+#undef TG_K2_CASE
+  check(false, "no slab-staged K2 instance for this (tu, wh)");
+}
+
+void forward_slab(tg_cone_plan& p, uint64_t view0, uint64_t nviews, const float* d_vol,
+                  float* d_out, cudaStream_t st, bool prep) {
+  const int nx = int(p.vol.shape[0]), ny = int(p.vol.shape[1]), nz = int(p.vol.shape[2]);
+  p.vt_order.enter(st);
+  const int vt_pitch = (ny + 3) & ~3;
+  const size_t vt_need = size_t(nz) * nx * vt_pitch;
+  const bool need_vx = (nx % 4) != 0 || (reinterpret_cast<uintptr_t>(d_vol) % 16) != 0;
+  const int vx_pitch = (nx + 3) & ~3;
+  const size_t vx_need = need_vx ? size_t(nz) * ny * vx_pitch : 0;
+  if (p.vt_elems < vt_need) {
+    if (p.d_vt) {
+      TG_CUDA(cudaStreamSynchronize(st));
+      TG_CUDA(cudaFree(p.d_vt));
+      p.d_vt = nullptr;
+    }
+    TG_CUDA(cudaMalloc(&p.d_vt, vt_need * sizeof(float)));
+    p.vt_elems = vt_need;
+    prep = true;
+  }
+  if (p.vx_elems < vx_need) {
+    if (p.d_vx) {
+      TG_CUDA(cudaStreamSynchronize(st));
+      TG_CUDA(cudaFree(p.d_vx));
+      p.d_vx = nullptr;
+    }
+    TG_CUDA(cudaMalloc(&p.d_vx, vx_need * sizeof(float)));
+    p.vx_elems = vx_need;
+    prep = true;
+  }
+  p.vt_pitch = vt_pitch;
+  p.vx_pitch = vx_pitch;
+  if (prep) {
+    dim3 tg((nx + 31) / 32, (vt_pitch + 31) / 32, nz);
+    transpose_xy_kernel<<<tg, dim3(32, 8), 0, st>>>(d_vol, p.d_vt, nx, ny, vt_pitch);
+    TG_LAUNCHED(1);
+    if (need_vx) {
+      repitch_x_kernel<<<148 * 8, 256, 0, st>>>(d_vol, p.d_vx, nx, nz * ny, vx_pitch);
+      TG_LAUNCHED(1);
+    }
+  }
+  if (!p.k2box.sized) k2_size_boxes(p);
+  const auto& B = p.k2box;
+  CUtensorMap mx, my;
+  const float* vxb = need_vx ? p.d_vx : d_vol;
+  const int xp = need_vx ? vx_pitch : nx;
+  // boxes laid out [dominant][z][transverse]: the maps walk (h, z, d) with
+  // permuted strides over V[z][y][x] (h = x, d = y) and Vt[z][x][y] (h = y, d = x)
+  check(encode_tensor_map_3d_f32(&mx, vxb, nx, nz, ny, uint64_t(xp) * ny * 4, uint64_t(xp) * 4,
+                                 B.wh, B.hz, B.t + 2) == CUDA_SUCCESS,
+        "cuTensorMapEncodeTiled failed (K2 x-fastest volume)");
+  check(encode_tensor_map_3d_f32(&my, p.d_vt, ny, nz, nx, uint64_t(vt_pitch) * nx * 4,
+                                 uint64_t(vt_pitch) * 4, B.wh, B.hz, B.t + 2) == CUDA_SUCCESS,
+        "cuTensorMapEncodeTiled failed (K2 y-fastest volume)");
+  fps::Args a{};
+  a.f = fp_args(p);
+  a.vol = d_vol;
+  a.boxZ = B.hz;
+  a.T = B.t;
+  a.stages = B.stages;
+  const bool stats = env_int("TG_K2_STATS", 0) != 0;
+  if (stats) {
+    if (!p.d_k2_stats) TG_CUDA(cudaMalloc(&p.d_k2_stats, 4 * sizeof(unsigned long long)));
+    TG_CUDA(cudaMemsetAsync(p.d_k2_stats, 0, 4 * sizeof(unsigned long long), st));
+    a.stats = p.d_k2_stats;
+  }
+  const size_t stage_elems = size_t((B.wh * (B.t + 2) * B.hz + 31) & ~31);
+  const size_t smem = stage_elems * 4 * B.stages + sizeof(fps::RayState) +
+                      sizeof(fps::StageHdr) * fps::MAX_STAGES + sizeof(fps::CtaHdr) +
+                      2 * fps::MAX_STAGES * sizeof(uint64_t);
+  const int TV = fps::NCONS / B.tu;
+  KernelTimer timer;
+  timer.start(st);
+  for (uint64_t c0 = 0; c0 < nviews; c0 += 65535) {
+    const uint64_t cn = std::min<uint64_t>(65535, nviews - c0);
+    a.f.view0 = int(view0 + c0);
+    a.f.out = d_out + c0 * p.det.n_u * p.det.n_v;
+    dim3 grid((a.f.nu + B.tu - 1) / B.tu, unsigned(cn), (a.f.nv + TV - 1) / TV);
+    launch_fp_slab(B.tu, B.wh, mx, my, a, grid, smem, st);
+    TG_LAUNCHED(1);
+  }
+  timer.stop();
+  if (stats) {
+    unsigned long long h[4];
+    TG_CUDA(cudaMemcpyAsync(h, p.d_k2_stats, sizeof h, cudaMemcpyDeviceToHost, st));
+    TG_CUDA(cudaStreamSynchronize(st));
+    std::fprintf(stderr, "[k2] slabs %llu global-slabs %llu global-ctas %llu\n", h[0], h[1], h[2]);
+  }
+  p.vt_order.leave(st);
+}
+
 void forward_impl(tg_cone_plan& p, uint64_t view0, uint64_t nviews, const float* d_vol,
                   float* d_out, cudaStream_t st, bool pad = true) {
   check(view0 + nviews <= p.n_proj && nviews >= 1, "view range lies outside the geometry");
   DeviceGuard dg(p.device);
   std::lock_guard<std::recursive_mutex> lk(p.mu);
+  if (p.k2_impl == 1) {
+    forward_slab(p, view0, nviews, d_vol, d_out, st, pad);
+    return;
+  }
   p.vpad_order.enter(st);
   ensure_vpad(p, st);
   const int nx = int(p.vol.shape[0]), ny = int(p.vol.shape[1]), nz = int(p.vol.shape[2]);
@@ -1557,6 +1841,9 @@ tg_status tg_cone_plan_destroy(tg_cone_plan* p) {
     cudaFree(p->d_cos);
     cudaFree(p->d_parker);
     cudaFree(p->d_vpad);
+    cudaFree(p->d_vt);
+    cudaFree(p->d_vx);
+    cudaFree(p->d_k2_stats);
     cudaFree(p->d_pitched);
     cudaFree(p->d_stage_in);
     cudaFree(p->d_stage_out);
@@ -1611,6 +1898,10 @@ tg_status tg_cone_plan_set_knob(tg_cone_plan* p, const char* name, int64_t value
     if (k == "k2_tu") {
       check(value == 32 || value == 64, "k2_tu must be 32 or 64");
       p->k2_tu = int(value);
+    } else if (k == "k2_impl") {
+      // 1: slab-staged K2 (shared-memory boxes, default); 0: quad-volume L1 gathers
+      check(value == 0 || value == 1, "k2_impl must be 0 or 1");
+      p->k2_impl = int(value);
     } else if (k == "k2_dual") {
       // 0: gather every ray from the x-fastest quad volume (bitwise identical)
       p->k2_dual_allowed = value != 0;

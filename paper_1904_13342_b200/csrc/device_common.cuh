@@ -145,7 +145,7 @@ uint64_t next_plan_id();
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
 CUresult encode_tensor_map_3d_f32(CUtensorMap* map, const void* base, uint64_t d0, uint64_t d1,
                                   uint64_t d2, uint64_t stride1_bytes, uint64_t stride2_bytes,
-                                  uint32_t box0, uint32_t box1);
+                                  uint32_t box0, uint32_t box1, uint32_t box2 = 1);
 
 // ---- device-side PTX helpers (sm_90+/sm_100a) --------------------------------
 

@@ -45,7 +45,7 @@ void KernelTimer::stop() {
 
 CUresult encode_tensor_map_3d_f32(CUtensorMap* map, const void* base, uint64_t d0, uint64_t d1,
                                   uint64_t d2, uint64_t stride1_bytes, uint64_t stride2_bytes,
-                                  uint32_t box0, uint32_t box1) {
+                                  uint32_t box0, uint32_t box1, uint32_t box2) {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
     void* p = nullptr;
     cudaDriverEntryPointQueryResult q;
@@ -58,7 +58,7 @@ CUresult encode_tensor_map_3d_f32(CUtensorMap* map, const void* base, uint64_t d
   if (!fn) return CUDA_ERROR_NOT_SUPPORTED;
   const cuuint64_t dims[3] = {d0, d1, d2};
   const cuuint64_t strides[2] = {stride1_bytes, stride2_bytes};
-  const cuuint32_t box[3] = {box0, box1, 1};
+  const cuuint32_t box[3] = {box0, box1, box2};
   const cuuint32_t elem[3] = {1, 1, 1};
   return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(base), dims, strides, box,
             elem, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,

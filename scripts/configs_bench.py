@@ -64,6 +64,8 @@ def main():
         r.update({"ref_fp_s": cpu_s(lambda: O.Ref.planar_forward(og, img)),
                   "ref_bp_s": cpu_s(lambda: O.Ref.planar_backproject(og, sn)),
                   "ref_fbp_s": cpu_s(lambda: O.Ref.fbp_reconstruct(og, sn))})
+    r["fp_gsamples_s"] = 4.761e7 / (r["fp_ms"] / 1e3) / 1e9
+    r["bp_gups"] = 256 * 256 * 360 / (r["bp_ms"] / 1e3) / 1e9
     out["c1_parallel_256"] = r
 
     # c2 fan
@@ -80,6 +82,8 @@ def main():
         sn = s2.data.cpu().numpy()
         r.update({"ref_fp_s": cpu_s(lambda: O.Ref.planar_forward(og, img)),
                   "ref_bp_s": cpu_s(lambda: O.Ref.planar_backproject(og, sn))})
+    r["fp_gsamples_s"] = 1.924e8 / (r["fp_ms"] / 1e3) / 1e9
+    r["bp_gups"] = 512 * 512 * 360 / (r["bp_ms"] / 1e3) / 1e9
     out["c2_fan_512"] = r
 
     # c3 cone FDK short scan

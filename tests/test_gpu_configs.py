@@ -163,25 +163,65 @@ K2_CASES = {
 
 
 @pytest.mark.parametrize("case", list(K2_CASES))
-def test_k2_band_variants_bitwise(tg, O, case):
-    """cone_fp_kernel<64> (4-row bands, chosen for quad slices >= 8 MB, e.g. c5)
-    and <32> give the same bits: the band shape only reorders rays over CTAs.
-    The x-fastest-only fallback (k2_dual 0) gathers the same taps too."""
+def test_k2_variants_bitwise(tg, O, case):
+    """The slab-staged K2 (k2_impl 1, shared-memory boxes) and the quad-volume
+    K2 (k2_impl 0) through both of its band heights (cone_fp_kernel<64> /
+    <32>) and without its y-fastest copy (k2_dual 0) give the same bits: the
+    sample positions and summation order are the same, only the tap source and
+    the ray-to-CTA assignment differ."""
     c = K2_CASES[case]
     geo, og = cone_pair(tg, O, **c)
     v = rand(og.vol_shape_zyx, 5)
     img = tg.Image(geo.volume, torch.from_numpy(v).to(DEV))
     outs = {}
+    tg.set_cone_knob(geo, "k2_impl", 0)
     for tu, dual in [(32, 1), (64, 1), (64, 0), (32, 0)]:
         tg.set_cone_knob(geo, "k2_tu", tu)
         tg.set_cone_knob(geo, "k2_dual", dual)
-        outs[(tu, dual)] = tg.forward_project(img, geo).data.cpu().numpy()
+        outs[(0, tu, dual)] = tg.forward_project(img, geo).data.cpu().numpy()
     tg.set_cone_knob(geo, "k2_tu", 32)
     tg.set_cone_knob(geo, "k2_dual", 1)
+    tg.set_cone_knob(geo, "k2_impl", 1)
+    outs[(1,)] = tg.forward_project(img, geo).data.cpu().numpy()
     ref = O.cone_forward(og, v)
-    assert_close(outs[(64, 1)], ref, what=f"K2<64> {case}")
+    assert_close(outs[(1,)], ref, what=f"K2 slab {case}")
+    assert_close(outs[(0, 64, 1)], ref, what=f"K2<64> {case}")
     for k, o in outs.items():
-        assert np.array_equal(o, outs[(32, 1)]), k
+        assert np.array_equal(o, outs[(1,)]), k
+
+
+def test_k2_slab_fallback_paths_bitwise(tg, O, monkeypatch):
+    """The slab-staged K2's fallbacks give the same bits as its shared-memory
+    path: (1) boxes forced too small (every slab gathers from global memory),
+    (2) z-dominant rays (calibrated matrices with x and z swapped: no x/y
+    dominant axis, the CTA marches in one global pass)."""
+    c = K2_CASES["shipped"]
+    geo, og = cone_pair(tg, O, **c)
+    v = rand(og.vol_shape_zyx, 9)
+    img = tg.Image(geo.volume, torch.from_numpy(v).to(DEV))
+    want = tg.forward_project(img, geo).data.cpu().numpy()
+    monkeypatch.setenv("TG_K2_HZ", "4")
+    geo_s, _ = cone_pair(tg, O, **c)  # fresh plan: boxes sized at its first forward
+    got = tg.forward_project(img, geo_s).data.cpu().numpy()
+    monkeypatch.delenv("TG_K2_HZ")
+    assert np.array_equal(got, want)
+    # z-dominant: permute the x and z columns of every projection matrix
+    vol = tg.VolumeSpec.centered([40, 40, 40], [1.0] * 3)
+    det = tg.Detector2D.centered(64, 64, 1.2, 1.2)
+    base = tg.make_cone(vol, det, 24, 2 * math.pi, 200.0, 400.0)
+    m = base.matrices.reshape(-1, 3, 4).copy()
+    m[:, :, [0, 2]] = m[:, :, [2, 0]]
+    mats = m.reshape(base.matrices.shape)
+    from _helpers import cone_pair_from_matrices
+    geo_z, og_z = cone_pair_from_matrices(tg, O, vol, det, 2 * math.pi, 200.0, 400.0, mats)
+    vz = rand(og_z.vol_shape_zyx, 10)
+    imz = tg.Image(geo_z.volume, torch.from_numpy(vz).to(DEV))
+    tg.set_cone_knob(geo_z, "k2_impl", 1)
+    slab = tg.forward_project(imz, geo_z).data.cpu().numpy()
+    tg.set_cone_knob(geo_z, "k2_impl", 0)
+    quad = tg.forward_project(imz, geo_z).data.cpu().numpy()
+    assert np.array_equal(slab, quad)
+    assert_close(slab, O.cone_forward(og_z, vz), what="K2 z-dominant")
 
 
 # ---- c5 sampled -------------------------------------------------------------------
@@ -195,8 +235,9 @@ def c5(tg):
 
 
 def test_c5_forward_views(tg, O, c5):
-    """K2 at c5 (the plan picks the 4-row-band cone_fp_kernel<64>): two views
-    of the 1024^3 Shepp-Logan against the oracle, exact zero pattern"""
+    """K2 at c5 (slab-staged; its 72-wide boxes where the plan's sizing picks
+    them): two views of the 1024^3 Shepp-Logan against the oracle, exact zero
+    pattern"""
     ph = tg.shepp_logan_3d(c5.volume, device=DEV).data
     views = [5, 410]
     out = torch.stack([tg.cone_forward_views(c5, ph, v, 1)[0] for v in views]).cpu().numpy()

@@ -75,6 +75,7 @@ def test_k2_single_layout_fallback_is_bitwise_equal(tg, O):
     det = tg.Detector2D.centered(120, 100, 1.2, 1.2)
     ph = tg.shepp_logan_3d(vol, device=DEV)
     geo_a = tg.make_cone(vol, det, 40, 2 * math.pi, 300.0, 600.0)
+    tg.set_cone_knob(geo_a, "k2_impl", 0)  # the quad-volume K2
     want = tg.forward_project(ph, geo_a).data.clone()
     one = 100 * 92 * 84 * 16  # one quad layout, bytes
     torch.cuda.synchronize()
@@ -85,6 +86,7 @@ def test_k2_single_layout_fallback_is_bitwise_equal(tg, O):
                       device=DEV)
     try:
         geo_b = tg.make_cone(vol, det, 40, 2 * math.pi, 300.0, 600.0)  # fresh plan
+        tg.set_cone_knob(geo_b, "k2_impl", 0)
         got = tg.forward_project(ph, geo_b).data.clone()
     finally:
         del hog
