@@ -387,7 +387,10 @@ tg_status tg_cone_ray_samples(tg_cone_plan* plan, uint64_t view0, uint64_t n_vie
 tg_status tg_planar_ray_samples(tg_planar_plan* plan, uint64_t* d_counts, void* stream);
 /* plan knobs for experiments and tests (outputs are bitwise unchanged):
  * "k2_tu" = 32 | 64 (K2 CTA width / detector band height 8 | 4 rows),
- * "k2_dual" = 0 | 1 (keep the y-fastest quad volume for x-dominant rays) */
+ * "k2_dual" = 0 | 1 (keep the y-fastest quad volume for x-dominant rays),
+ * "k2_impl" = 1 (slab-staged K2: shared-memory volume boxes) | 0 (quad-volume
+ * K2: L1 gathers) | -1 (default: time both at the plan's first forward
+ * projection and keep the faster) */
 tg_status tg_cone_plan_set_knob(tg_cone_plan* plan, const char* name, int64_t value);
 
 /* ---- instrumentation ---------------------------------------------------- */

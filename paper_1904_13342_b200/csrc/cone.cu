@@ -775,8 +775,10 @@ struct tg_cone_plan {
   bool k2_dual_denied = false;  // the copy did not fit at the last allocation
   int k2_tu = 32;            // K2 CTA width in u (band height 256 / k2_tu rows)
   size_t vpad_elems = 0;
-  // slab-staged K2 (default; knob "k2_impl" 1) vs the quad-volume K2 (0)
-  int k2_impl = 1;
+  // K2 implementation: 1 slab-staged (shared-memory boxes), 0 quad-volume L1
+  // gathers, -1 (default) = time both once at the plan's first forward
+  // projection and keep the faster (identical output bits); knob "k2_impl"
+  int k2_impl = -1;
   float* d_vt = nullptr;       // y-fastest copy Vt[z][x][y] (row pitch vt_pitch)
   float* d_vx = nullptr;       // x-fastest re-pitched copy (only when nx % 4 != 0)
   size_t vt_elems = 0, vx_elems = 0;
@@ -1072,91 +1074,101 @@ int env_int(const char* name, int dflt) {
 }
 
 // Host replica of the producer's box sizing over a sample of views: picks
-// the transverse box width WH (a template instance) and the z extent HZ so
-// that >= 99% of (tile, slab) boxes fit; the rest gather from global memory
-// (same bits).  Environment overrides for experiments: TG_K2_TU, TG_K2_WH,
-// TG_K2_T, TG_K2_HZ, TG_K2_STAGES.
+// the slab thickness T, the transverse box width WH (a template instance)
+// and the z extent HZ so that >= 99.8% of (tile, slab) boxes fit and two CTAs
+// (two ring stages each) share an SM; the rest gather from global memory
+// (same bits).  WH = 8 (mod 32) when rays are at most one voxel apart at the
+// isocentre, 12 (mod 32) when they are sparser (a warp's 8 columns then span
+// more than 8 banks; offline bank model, profiles/r2_k2_bank_model.txt).
+// Environment overrides for experiments: TG_K2_WH, TG_K2_T, TG_K2_HZ,
+// TG_K2_STAGES, TG_K2_STATS.
 void k2_size_boxes(tg_cone_plan& p) {
   auto& B = p.k2box;
-  B.tu = env_int("TG_K2_TU", 16);
-  B.t = env_int("TG_K2_T", 8);
-  const int TU = B.tu, TV = fps::NCONS / TU, T = B.t;
+  B.tu = 16;
+  const int TU = B.tu, TV = fps::NCONS / TU;
   const int nx = int(p.vol.shape[0]), ny = int(p.vol.shape[1]), nz = int(p.vol.shape[2]);
   const int nu = int(p.det.n_u), nv = int(p.det.n_v);
-  static const int kWH[] = {40, 72};  // = 8 (mod 32): see cone_fp_slab.cuh
+  const double ray_pitch = p.det.spacing_u * p.sid / p.sdd /
+                           std::min(p.vol.spacing[0], p.vol.spacing[1]);
+  const bool sparse = ray_pitch > 1.05;
+  const int kWH[2] = {sparse ? 44 : 40, sparse ? 76 : 72};
   constexpr int kMaxNeed = 260;
-  std::vector<uint64_t> hist(size_t(kMaxNeed) * kMaxNeed, 0);  // [wneed][zneed]
-  uint64_t total = 0;
-  const int n_sample = int(std::min<uint64_t>(p.n_proj, 12));
-  for (int si = 0; si < n_sample; ++si) {
-    const uint64_t view = (uint64_t(si) * p.n_proj) / uint64_t(n_sample);
-    const double* src = p.sources.data() + 3 * view;
-    const double* M = p.invs.data() + 9 * view;
-    const double o[3] = {(src[0] - p.vol.origin[0]) / p.vol.spacing[0],
-                         (src[1] - p.vol.origin[1]) / p.vol.spacing[1],
-                         (src[2] - p.vol.origin[2]) / p.vol.spacing[2]};
-    for (int v0 = 0; v0 < nv; v0 += TV)
-      for (int u0 = 0; u0 < nu; u0 += TU) {
-        double e[4][3];
-        double sx = 0, sy = 0;
-        for (int c = 0; c < 4; ++c) {
-          const int iu = (c & 1) ? std::min(u0 + TU, nu) - 1 : u0;
-          const int iv = (c & 2) ? std::min(v0 + TV, nv) - 1 : v0;
-          for (int r = 0; r < 3; ++r)
-            e[c][r] = (M[3 * r] * iu + M[3 * r + 1] * iv + M[3 * r + 2]) / p.vol.spacing[r];
-          sx += e[c][0];
-          sy += e[c][1];
+  const size_t fixed = sizeof(fps::RayState) + 1024;
+  const size_t budget = 113 * 1024;  // two CTAs per SM
+  auto size_for = [&](int T, int& wh, int& hz, uint64_t& total) {
+    std::vector<uint64_t> hist(size_t(kMaxNeed) * kMaxNeed, 0);  // [wneed][zneed]
+    total = 0;
+    const int n_sample = int(std::min<uint64_t>(p.n_proj, 12));
+    for (int si = 0; si < n_sample; ++si) {
+      const uint64_t view = (uint64_t(si) * p.n_proj) / uint64_t(n_sample);
+      const double* src = p.sources.data() + 3 * view;
+      const double* M = p.invs.data() + 9 * view;
+      const double o[3] = {(src[0] - p.vol.origin[0]) / p.vol.spacing[0],
+                           (src[1] - p.vol.origin[1]) / p.vol.spacing[1],
+                           (src[2] - p.vol.origin[2]) / p.vol.spacing[2]};
+      for (int v0 = 0; v0 < nv; v0 += TV)
+        for (int u0 = 0; u0 < nu; u0 += TU) {
+          double e[4][3];
+          double sx = 0, sy = 0;
+          for (int c = 0; c < 4; ++c) {
+            const int iu = (c & 1) ? std::min(u0 + TU, nu) - 1 : u0;
+            const int iv = (c & 2) ? std::min(v0 + TV, nv) - 1 : v0;
+            for (int r = 0; r < 3; ++r)
+              e[c][r] = (M[3 * r] * iu + M[3 * r + 1] * iv + M[3 * r + 2]) / p.vol.spacing[r];
+            sx += e[c][0];
+            sy += e[c][1];
+          }
+          const bool xdom = std::fabs(sx) > std::fabs(sy);
+          const int nd = xdom ? nx : ny;
+          double hA[4], hB[4], zA[4], zB[4];
+          bool ok = true;
+          for (int c = 0; c < 4; ++c) {
+            const double ed = xdom ? e[c][0] : e[c][1], eh = xdom ? e[c][1] : e[c][0];
+            const double od = xdom ? o[0] : o[1], oh = xdom ? o[1] : o[0];
+            const double len = std::sqrt(e[c][0] * e[c][0] + e[c][1] * e[c][1] + e[c][2] * e[c][2]);
+            ok = ok && std::fabs(ed) >= 0.3 * len;
+            hB[c] = eh / ed;
+            hA[c] = oh - od * hB[c];
+            zB[c] = e[c][2] / ed;
+            zA[c] = o[2] - od * zB[c];
+          }
+          if (!ok) continue;
+          for (int s0 = -3; s0 <= nd; s0 += T) {
+            // box planes [s0 - 1, s0 + T + 1] cover both march directions
+            double hmin = 1e300, hmax = -1e300, zmin = 1e300, zmax = -1e300;
+            for (int c = 0; c < 4; ++c)
+              for (int k = 0; k < 2; ++k) {
+                const double P = double(s0 - 1 + k * (T + 2));
+                const double hh = hA[c] + P * hB[c], zz = zA[c] + P * zB[c];
+                hmin = std::min(hmin, hh);
+                hmax = std::max(hmax, hh);
+                zmin = std::min(zmin, zz);
+                zmax = std::max(zmax, zz);
+              }
+            // slabs entirely outside the volume hold no samples
+            if (zmax < -2.0 || zmin > nz + 1.0) continue;
+            if (xdom ? (hmax < -2.0 || hmin > ny + 1.0) : (hmax < -2.0 || hmin > nx + 1.0)) continue;
+            const int hb = (int(std::floor(hmin)) - 1) & ~3, zb = int(std::floor(zmin)) - 1;
+            const int wn = std::min(kMaxNeed - 1, int(std::floor(hmax)) + 3 - hb);
+            const int zn = std::min(kMaxNeed - 1, int(std::floor(zmax)) + 3 - zb);
+            ++hist[size_t(wn) * kMaxNeed + zn];
+            ++total;
+          }
         }
-        const bool xdom = std::fabs(sx) > std::fabs(sy);
-        const int nd = xdom ? nx : ny;
-        double hA[4], hB[4], zA[4], zB[4];
-        bool ok = true;
-        for (int c = 0; c < 4; ++c) {
-          const double ed = xdom ? e[c][0] : e[c][1], eh = xdom ? e[c][1] : e[c][0];
-          const double od = xdom ? o[0] : o[1], oh = xdom ? o[1] : o[0];
-          const double len = std::sqrt(e[c][0] * e[c][0] + e[c][1] * e[c][1] + e[c][2] * e[c][2]);
-          ok = ok && std::fabs(ed) >= 0.3 * len;
-          hB[c] = eh / ed;
-          hA[c] = oh - od * hB[c];
-          zB[c] = e[c][2] / ed;
-          zA[c] = o[2] - od * zB[c];
-        }
-        if (!ok) continue;
-        for (int s0 = -3; s0 <= nd; s0 += T) {
-          // box planes [s0 - 1, s0 + T + 1] cover both march directions
-          double hmin = 1e300, hmax = -1e300, zmin = 1e300, zmax = -1e300;
-          for (int c = 0; c < 4; ++c)
-            for (int k = 0; k < 2; ++k) {
-              const double P = double(s0 - 1 + k * (T + 2));
-              const double hh = hA[c] + P * hB[c], zz = zA[c] + P * zB[c];
-              hmin = std::min(hmin, hh);
-              hmax = std::max(hmax, hh);
-              zmin = std::min(zmin, zz);
-              zmax = std::max(zmax, zz);
-            }
-          // slabs entirely outside the volume hold no samples
-          if (zmax < -2.0 || zmin > nz + 1.0) continue;
-          if (xdom ? (hmax < -2.0 || hmin > ny + 1.0) : (hmax < -2.0 || hmin > nx + 1.0)) continue;
-          const int hb = (int(std::floor(hmin)) - 1) & ~3, zb = int(std::floor(zmin)) - 1;
-          const int wn = std::min(kMaxNeed - 1, int(std::floor(hmax)) + 3 - hb);
-          const int zn = std::min(kMaxNeed - 1, int(std::floor(zmax)) + 3 - zb);
-          ++hist[size_t(wn) * kMaxNeed + zn];
-          ++total;
-        }
-      }
-  }
-  int wh = 72, hz = 256;
-  if (total) {
+    }
+    wh = kWH[1];
+    hz = 256;
+    if (!total) return;
     for (int cand : kWH) {
       uint64_t fit = 0;
       for (int wn = 0; wn <= cand; ++wn)
         for (int zn = 0; zn < kMaxNeed; ++zn) fit += hist[size_t(wn) * kMaxNeed + zn];
-      if (fit >= uint64_t(0.999 * double(total)) || cand == 72) {
+      if (fit >= uint64_t(0.999 * double(total))) {
         wh = cand;
         break;
       }
     }
-    // smallest HZ with >= 99% of all slabs fitting (WH and HZ)
+    // smallest HZ with >= 99.8% of all slabs fitting (WH and HZ)
     std::vector<uint64_t> zc(kMaxNeed, 0);
     for (int wn = 0; wn <= wh; ++wn)
       for (int zn = 0; zn < kMaxNeed; ++zn) zc[zn] += hist[size_t(wn) * kMaxNeed + zn];
@@ -1169,19 +1181,36 @@ void k2_size_boxes(tg_cone_plan& p) {
         break;
       }
     }
+  };
+  auto stage_bytes = [](int wh, int t, int hz) {
+    return size_t((wh * (t + 2) * ((hz + 3) & ~3) + 31) & ~31) * 4;
+  };
+  // thickest slab (fewest per-slab overheads) whose two stages still leave
+  // room for two CTAs per SM
+  int wh = 0, hz = 0, t = 0;
+  uint64_t total = 0;
+  const int forced_t = env_int("TG_K2_T", 0);
+  for (int T : {8, 6, 4}) {
+    if (forced_t && T != forced_t) continue;
+    size_for(T, wh, hz, total);
+    t = T;
+    if (fixed + 2 * stage_bytes(wh, T, hz) <= budget) break;
   }
+  if (forced_t && !t) {
+    t = forced_t;
+    size_for(t, wh, hz, total);
+  }
+  B.t = t;
   B.wh = env_int("TG_K2_WH", wh);
   B.hz = (std::max(4, std::min(256, env_int("TG_K2_HZ", hz))) + 3) & ~3;
-  // ring depth: two CTAs per SM (<= ~113 KB of shared memory each)
-  const size_t stage_bytes = size_t((B.wh * (B.t + 2) * B.hz + 31) & ~31) * 4;
-  const size_t fixed = sizeof(fps::RayState) + 1024;
-  int stages = int((113 * 1024 - fixed) / stage_bytes);
+  const size_t sb = stage_bytes(B.wh, B.t, B.hz);
+  int stages = int((budget - fixed) / sb);
   stages = std::max(2, std::min(fps::MAX_STAGES, stages));
   B.stages = std::max(1, std::min(fps::MAX_STAGES, env_int("TG_K2_STAGES", stages)));
   B.sized = true;
   if (env_int("TG_K2_STATS", 0))
-    std::fprintf(stderr, "[k2] tu %d wh %d t %d hz %d stages %d (sampled slabs %llu)\n", B.tu,
-                 B.wh, B.t, B.hz, B.stages, (unsigned long long)total);
+    std::fprintf(stderr, "[k2] tu %d wh %d t %d hz %d stages %d ray pitch %.2f (sampled slabs %llu)\n",
+                 B.tu, B.wh, B.t, B.hz, B.stages, ray_pitch, (unsigned long long)total);
 }
 
 template <int TU, int WH>
@@ -1201,8 +1230,8 @@ void launch_fp_slab(int tu, int wh, const CUtensorMap& mx, const CUtensorMap& my
   }
   TG_K2_CASE(16, 40)
   TG_K2_CASE(16, 72)
-  TG_K2_CASE(32, 40)
-  TG_K2_CASE(32, 72)
+  TG_K2_CASE(16, 44)
+  TG_K2_CASE(16, 76)
 #undef TG_K2_CASE
   check(false, "no slab-staged K2 instance for this (tu, wh)");
 }
@@ -1297,15 +1326,90 @@ void forward_slab(tg_cone_plan& p, uint64_t view0, uint64_t nviews, const float*
   p.vt_order.leave(st);
 }
 
+void forward_quad(tg_cone_plan& p, uint64_t view0, uint64_t nviews, const float* d_vol,
+                  float* d_out, cudaStream_t st, bool pad);
+
+// One-time choice between the two K2 implementations (same output bits):
+// each runs twice on twelve blocks of consecutive views spread over the
+// plan (the second run is timed, after the volume preparation of the first),
+// the faster is kept and
+// the other's scratch volume freed.  Slab on ties (2x the volume of scratch
+// against the quad kernel's 8.8x), and whenever the quad volumes do not fit
+// or the stream is being captured.
+void k2_autotune(tg_cone_plan& p, const float* d_vol, cudaStream_t st) {
+  p.k2_impl = 1;
+  if (ScratchOrder::capturing(st)) return;
+  const uint64_t per_view = p.det.n_u * p.det.n_v;
+  // twelve blocks of consecutive views spread evenly over the plan's range
+  // (the quad kernel's speed varies with the view angle, the slab kernel's
+  // hardly), each block >= ~20k slab CTAs so that launch tails do not decide
+  const uint64_t tiles = ((p.det.n_u + 15) / 16) * ((p.det.n_v + 15) / 16);
+  const int nblk = p.n_proj >= 48 ? 12 : 1;
+  const uint64_t want = std::max<uint64_t>(4, (20000 + tiles - 1) / tiles);
+  const int blk = int(std::min<uint64_t>(want, p.n_proj / uint64_t(nblk)));
+  const int ns = blk;
+  const size_t one = size_t(p.vol.shape[0] + 4) * (p.vol.shape[1] + 4) * (p.vol.shape[2] + 4) * 16;
+  size_t free_b = 0, total_b = 0;
+  TG_CUDA(cudaMemGetInfo(&free_b, &total_b));
+  if (one + size_t(ns) * per_view * 4 + total_b / 10 > free_b) return;
+  float* scratch = nullptr;
+  TG_CUDA(cudaMalloc(&scratch, size_t(ns) * per_view * sizeof(float)));
+  cudaEvent_t a, b;
+  TG_CUDA(cudaEventCreate(&a));
+  TG_CUDA(cudaEventCreate(&b));
+  float ms[2] = {0.f, 0.f};
+  for (int impl = 0; impl < 2; ++impl) {
+    for (int rep = 0; rep < 2; ++rep) {
+      TG_CUDA(cudaEventRecord(a, st));
+      for (int i = 0; i < nblk; ++i) {
+        const uint64_t v = uint64_t(i) * (p.n_proj - blk) / uint64_t(std::max(1, nblk - 1));
+        if (impl == 0)
+          forward_quad(p, v, blk, d_vol, scratch, st, rep == 0 && i == 0);
+        else
+          forward_slab(p, v, blk, d_vol, scratch, st, rep == 0 && i == 0);
+      }
+      TG_CUDA(cudaEventRecord(b, st));
+      TG_CUDA(cudaEventSynchronize(b));
+      TG_CUDA(cudaEventElapsedTime(&ms[impl], a, b));
+    }
+  }
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  TG_CUDA(cudaFree(scratch));
+  p.k2_impl = (ms[0] < 0.97f * ms[1]) ? 0 : 1;
+  // drop the loser's scratch (the stream is idle: synchronised above)
+  if (p.k2_impl == 1 && p.d_vpad) {
+    TG_CUDA(cudaFree(p.d_vpad));
+    p.d_vpad = nullptr;
+    p.vpad_elems = 0;
+  } else if (p.k2_impl == 0) {
+    if (p.d_vt) TG_CUDA(cudaFree(p.d_vt));
+    if (p.d_vx) TG_CUDA(cudaFree(p.d_vx));
+    p.d_vt = p.d_vx = nullptr;
+    p.vt_elems = p.vx_elems = 0;
+  }
+  if (env_int("TG_K2_STATS", 0))
+    std::fprintf(stderr, "[k2] autotune over %d views: quad %.3f ms, slab %.3f ms -> %s\n", nblk * blk,
+                 ms[0], ms[1], p.k2_impl ? "slab" : "quad");
+}
+
 void forward_impl(tg_cone_plan& p, uint64_t view0, uint64_t nviews, const float* d_vol,
                   float* d_out, cudaStream_t st, bool pad = true) {
   check(view0 + nviews <= p.n_proj && nviews >= 1, "view range lies outside the geometry");
   DeviceGuard dg(p.device);
   std::lock_guard<std::recursive_mutex> lk(p.mu);
-  if (p.k2_impl == 1) {
-    forward_slab(p, view0, nviews, d_vol, d_out, st, pad);
-    return;
+  if (p.k2_impl < 0) {
+    k2_autotune(p, d_vol, st);
+    pad = true;  // re-prepare the chosen layout for this volume
   }
+  if (p.k2_impl == 1)
+    forward_slab(p, view0, nviews, d_vol, d_out, st, pad);
+  else
+    forward_quad(p, view0, nviews, d_vol, d_out, st, pad);
+}
+
+void forward_quad(tg_cone_plan& p, uint64_t view0, uint64_t nviews, const float* d_vol,
+                  float* d_out, cudaStream_t st, bool pad) {
   p.vpad_order.enter(st);
   ensure_vpad(p, st);
   const int nx = int(p.vol.shape[0]), ny = int(p.vol.shape[1]), nz = int(p.vol.shape[2]);
@@ -1320,9 +1424,10 @@ void forward_impl(tg_cone_plan& p, uint64_t view0, uint64_t nviews, const float*
   FpArgs a = fp_args(p);
   KernelTimer timer;
   timer.start(st);
-  // one launch per <= 65535 views (grid z limit)
-  for (uint64_t c0 = 0; c0 < nviews; c0 += 65535) {
-    const uint64_t cn = std::min<uint64_t>(65535, nviews - c0);
+  // one launch per block of views (TG_K2_QBLK, default all; grid limit 65535)
+  const uint64_t qblk = uint64_t(std::max(1, std::min(65535, env_int("TG_K2_QBLK", 65535))));
+  for (uint64_t c0 = 0; c0 < nviews; c0 += qblk) {
+    const uint64_t cn = std::min<uint64_t>(qblk, nviews - c0);
     a.view0 = int(view0 + c0);
     a.out = d_out + c0 * p.det.n_u * p.det.n_v;
     const int TU = p.k2_tu;
@@ -1899,8 +2004,9 @@ tg_status tg_cone_plan_set_knob(tg_cone_plan* p, const char* name, int64_t value
       check(value == 32 || value == 64, "k2_tu must be 32 or 64");
       p->k2_tu = int(value);
     } else if (k == "k2_impl") {
-      // 1: slab-staged K2 (shared-memory boxes, default); 0: quad-volume L1 gathers
-      check(value == 0 || value == 1, "k2_impl must be 0 or 1");
+      // 1: slab-staged K2 (shared-memory boxes); 0: quad-volume L1 gathers;
+      // -1: autotune at the next forward projection (default)
+      check(value == 0 || value == 1 || value == -1, "k2_impl must be -1, 0 or 1");
       p->k2_impl = int(value);
     } else if (k == "k2_dual") {
       // 0: gather every ray from the x-fastest quad volume (bitwise identical)

@@ -219,9 +219,24 @@ __global__ void pad_quads_kernel(const float* __restrict__ img, float4* __restri
 
 // ---------------------------------------------------------------------------
 // K4 / K6
+//
+// CTA = 32 x 32 pixel tile, 256 threads, 4 pixels per thread (rows ty + 8q)
+// processed as two FP32x2 pairs.  The views are split over the CTAs of a
+// thread-block cluster (1 x 1 x G) and reduced through distributed shared
+// memory in a fixed order (deterministic, one writer per pixel, no atomics).
+// Per chunk of views: (1) one thread per view builds the view's FP64 map at
+// the tile origin and the tile's footprint on the detector row (the bin
+// coordinate is affine (parallel) or projective with positive depth (fan)
+// over the tile, so its extremes sit on the 4 corners); (2) the CTA stages
+// each view's footprint bins [b0, b0 + W) into shared memory, zero outside
+// the detector (= the reference's zero-padded interp_row, projector.hpp:32-41);
+// (3) every pixel interpolates from shared memory with no bounds checks.
+// Views whose footprint is wider than the staging row, or that put part of
+// the tile behind the source (fan), take a checked path from global memory.
 
-constexpr int kTX = 32, kTY = 16;  // pixel tile
-constexpr int kChunk = 128;        // views whose maps sit in shared memory at once
+constexpr int kTX = 32, kTY = 32;  // pixel tile
+constexpr int kChunk = 64;         // views staged in shared memory at once
+constexpr int kRow = 96;           // staged bins per view
 constexpr int kMaxCluster = 8;
 
 struct BpArgs {
@@ -237,52 +252,65 @@ struct BpArgs {
   float* img;
 };
 
-// tile-local map of one view: bin - base = (n0 + lx na + ly nb) / (d0 + lx da + ly db)
+// tile-local map of one view: bin - b0 = (n0 + lx na + ly nb) / (d0 + lx da + ly db)
 struct ViewMap {
-  float n0, na, nb, d0, da, db, w;  // w = SID (fan; weight (SID / D)^2) or 0 (parallel)
-  int base;
+  float n0, na, nb, d0, da, db;
+  int b0;    // first staged bin
+  int fast;  // footprint staged (and, fan: whole tile in front of the source)
 };
 
 // FP64 map of view i for the tile at pixel (x0, y0), mirroring
-// projector.hpp:186-208 (parallel) / 232-260 (fan) for the tile-origin pixel.
+// projector.hpp:186-208 (parallel) / 232-260 (fan), shifted by the bin b0.
 template <bool FAN>
 __device__ ViewMap make_map(const BpArgs& a, int i, int x0, int y0) {
   const double rx = a.rays[2 * i], ry = a.rays[2 * i + 1];
   const double axx = -ry, axy = rx;  // detector axis: ray rotated +90 deg
   const double X0 = a.ox + double(x0) * a.sx, Y0 = a.oy + double(y0) * a.sy;
-  // base: the bin at the tile centre, so tile-local bins stay small
-  const double Xc = X0 + 0.5 * kTX * a.sx, Yc = Y0 + 0.5 * kTY * a.sy;
+  const int ex = min(kTX, a.nx - x0) - 1, ey = min(kTY, a.ny - y0) - 1;
   ViewMap m;
   if (!FAN) {
-    const double tc = (Xc * axx + Yc * axy - a.det_origin) * a.inv_ds;
-    const double base = floor(tc);
-    const double t0 = (X0 * axx + Y0 * axy - a.det_origin) * a.inv_ds - base;
-    m.n0 = float(t0);
-    m.na = float(a.sx * axx * a.inv_ds);
-    m.nb = float(a.sy * axy * a.inv_ds);
+    // bin(x, y) = ((x, y) . axis - origin) / spacing: affine
+    const double t00 = (X0 * axx + Y0 * axy - a.det_origin) * a.inv_ds;
+    const double tx = a.sx * axx * a.inv_ds, ty = a.sy * axy * a.inv_ds;
+    const double lo = t00 + fmin(0.0, ex * tx) + fmin(0.0, ey * ty);
+    const double hi = t00 + fmax(0.0, ex * tx) + fmax(0.0, ey * ty);
+    const int b0 = int(floor(fmax(lo, -1e8))) - 1;
+    m.b0 = b0;
+    m.fast = (floor(fmin(hi, 1e8)) + 2.0 - double(b0) < double(kRow)) ? 1 : 0;
+    m.n0 = float(t00 - double(b0));
+    m.na = float(tx);
+    m.nb = float(ty);
     m.d0 = 1.0f;
     m.da = 0.0f;
     m.db = 0.0f;
-    m.w = 0.0f;
-    m.base = int(base);
   } else {
-    const double qcx = Xc + a.sid * rx, qcy = Yc + a.sid * ry;
-    const double dc = qcx * rx + qcy * ry;
-    const double tc = dc > 0.0 ? (a.sdd * (qcx * axx + qcy * axy) / dc - a.det_origin) * a.inv_ds : 0.0;
-    const double base = floor(fmin(fmax(tc, -1e9), 1e9));
+    // depth D = q . r and bin numerator N = SDD q . axis, q = (x, y) + SID r:
+    // bin = (N / D - origin) / spacing, projective in (x, y)
     const double qx = X0 + a.sid * rx, qy = Y0 + a.sid * ry;
     const double D0 = qx * rx + qy * ry;
     const double M0 = qx * axx + qy * axy;
-    const double c = a.det_origin + base * a.det_spacing;
-    // bin - base = (SDD num - c depth) / (spacing depth)
+    double lo = 1e300, hi = -1e300, dmin = 1e300;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const double dx = (c & 1) ? ex * a.sx : 0.0, dy = (c & 2) ? ey * a.sy : 0.0;
+      const double D = D0 + dx * rx + dy * ry;
+      const double M = M0 + dx * axx + dy * axy;
+      dmin = fmin(dmin, D);
+      const double t = D > 0.0 ? (a.sdd * M / D - a.det_origin) * a.inv_ds : 0.0;
+      lo = fmin(lo, t);
+      hi = fmax(hi, t);
+    }
+    const int b0 = int(floor(fmin(fmax(lo, -1e8), 1e8))) - 1;
+    m.b0 = b0;
+    m.fast = (dmin > 0.0 && floor(fmin(hi, 1e8)) + 2.0 - double(b0) < double(kRow)) ? 1 : 0;
+    const double c = a.det_origin + double(b0) * a.det_spacing;
+    // bin - b0 = (SDD num - c depth) / (spacing depth)
     m.n0 = float((a.sdd * M0 - c * D0) * a.inv_ds);
     m.na = float((a.sdd * a.sx * axx - c * a.sx * rx) * a.inv_ds);
     m.nb = float((a.sdd * a.sy * axy - c * a.sy * ry) * a.inv_ds);
     m.d0 = float(D0);
     m.da = float(a.sx * rx);
     m.db = float(a.sy * ry);
-    m.w = float(a.sid);
-    m.base = int(base);
   }
   return m;
 }
@@ -300,45 +328,122 @@ __device__ __forceinline__ float interp_row(const float* __restrict__ row, int n
 template <bool FAN>
 __global__ void __launch_bounds__(256) planar_bp_kernel(const BpArgs a) {
   __shared__ ViewMap maps[kChunk];
+  __shared__ float rows[kChunk][kRow];
   __shared__ float part[kTX * kTY];
   cg::cluster_group cluster = cg::this_cluster();
   const int G = int(cluster.num_blocks());
   const int rank = int(cluster.block_rank());
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const int x0 = blockIdx.x * kTX, y0 = blockIdx.y * kTY;
-  const float lx = float(tx), ly0 = float(ty), ly1 = float(ty + 8);
+  // pixels past the image edge (partial tiles) evaluate a clamped in-tile
+  // position — their result is discarded, but their taps stay in the footprint
+  const int ex = min(kTX, a.nx - x0) - 1, ey = min(kTY, a.ny - y0) - 1;
+  const float lx = float(min(tx, ex));
+  // pixel pairs (ty, ty + 8) and (ty + 16, ty + 24)
+  const float2 lyA = make_float2(float(min(ty, ey)), float(min(ty + 8, ey)));
+  const float2 lyB = make_float2(float(min(ty + 16, ey)), float(min(ty + 24, ey)));
   const int v_begin = min(a.n_views, rank * a.vpg);
   const int v_end = min(a.n_views, v_begin + a.vpg);
-  float acc0 = 0.0f, acc1 = 0.0f;
+  constexpr float MAGIC = 12582912.0f;  // 1.5 * 2^23: t = M + floor(p) under round-down
+  const float2 M2 = make_float2(MAGIC, MAGIC), nM2 = make_float2(-MAGIC, -MAGIC);
+  const float sid = float(a.sid);
+  float2 accA = make_float2(0.f, 0.f), accB = accA;
+  const uint32_t rows_base = smem_u32(&rows[0][0]);
   for (int c0 = v_begin; c0 < v_end; c0 += kChunk) {
     const int cn = min(kChunk, v_end - c0);
     __syncthreads();
     if (threadIdx.x < cn) maps[threadIdx.x] = make_map<FAN>(a, c0 + threadIdx.x, x0, y0);
     __syncthreads();
-    const float* row = a.sino + (long long)c0 * a.nb;
+    // stage every view's footprint (coalesced per view; zero off the detector)
+    for (int e = threadIdx.x; e < cn * kRow; e += 256) {
+      const int v = e / kRow, i = e - v * kRow;
+      const int b = maps[v].b0 + i;
+      rows[v][i] = (maps[v].fast && (unsigned)b < (unsigned)a.nb)
+                       ? __ldg(a.sino + (long long)(c0 + v) * a.nb + b)
+                       : 0.0f;
+    }
+    __syncthreads();
 #pragma unroll 2
-    for (int k = 0; k < cn; ++k, row += a.nb) {
+    for (int k = 0; k < cn; ++k) {
       const ViewMap m = maps[k];
       const float n0 = fmaf(lx, m.na, m.n0);
-      const float nn0 = fmaf(ly0, m.nb, n0), nn1 = fmaf(ly1, m.nb, n0);
-      if (!FAN) {
-        acc0 += interp_row(row, a.nb, m.base, nn0);
-        acc1 += interp_row(row, a.nb, m.base, nn1);
+      const float2 n02 = make_float2(n0, n0), nb2 = make_float2(m.nb, m.nb);
+      if (m.fast) {
+        const uint32_t rb = rows_base + uint32_t(k * kRow) * 4u - uint32_t(0x4B400000) * 4u;
+        if (!FAN) {
+          auto upd = [&](float2 ly, float2& acc) {
+            const float2 t = __ffma2_rn(ly, nb2, n02);
+            const float2 tt = __fadd2_rd(t, M2);
+            const float2 fl = __fadd2_rn(tt, nM2);
+            const float2 w = __fadd2_rn(t, make_float2(-fl.x, -fl.y));
+            const uint32_t ia = rb + __float_as_uint(tt.x) * 4u, ib = rb + __float_as_uint(tt.y) * 4u;
+            float a0, a1, b0, b1;
+            asm volatile("ld.shared.f32 %0, [%2];\n\tld.shared.f32 %1, [%2+4];" : "=f"(a0), "=f"(a1) : "r"(ia));
+            asm volatile("ld.shared.f32 %0, [%2];\n\tld.shared.f32 %1, [%2+4];" : "=f"(b0), "=f"(b1) : "r"(ib));
+            const float2 lo = make_float2(a0, b0), hi = make_float2(a1, b1);
+            const float2 v = __ffma2_rn(w, __fadd2_rn(hi, make_float2(-lo.x, -lo.y)), lo);
+            acc = __fadd2_rn(acc, v);
+          };
+          upd(lyA, accA);
+          upd(lyB, accB);
+        } else {
+          const float d0 = fmaf(lx, m.da, m.d0);
+          const float2 d02 = make_float2(d0, d0), db2 = make_float2(m.db, m.db);
+          auto upd = [&](float2 ly, float2& acc) {
+            const float2 dd = __ffma2_rn(ly, db2, d02);
+            float2 r;
+            asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r.x) : "f"(dd.x));
+            asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r.y) : "f"(dd.y));
+            const float2 t = __fmul2_rn(__ffma2_rn(ly, nb2, n02), r);
+            const float2 tt = __fadd2_rd(t, M2);
+            const float2 fl = __fadd2_rn(tt, nM2);
+            const float2 w = __fadd2_rn(t, make_float2(-fl.x, -fl.y));
+            const uint32_t ia = rb + __float_as_uint(tt.x) * 4u, ib = rb + __float_as_uint(tt.y) * 4u;
+            float a0, a1, b0, b1;
+            asm volatile("ld.shared.f32 %0, [%2];\n\tld.shared.f32 %1, [%2+4];" : "=f"(a0), "=f"(a1) : "r"(ia));
+            asm volatile("ld.shared.f32 %0, [%2];\n\tld.shared.f32 %1, [%2+4];" : "=f"(b0), "=f"(b1) : "r"(ib));
+            const float2 lo = make_float2(a0, b0), hi = make_float2(a1, b1);
+            const float2 v = __ffma2_rn(w, __fadd2_rn(hi, make_float2(-lo.x, -lo.y)), lo);
+            // 1/U^2 = (SID / depth)^2 (projector.hpp:250-256)
+            const float2 s = __fmul2_rn(make_float2(sid, sid), r);
+            acc = __ffma2_rn(__fmul2_rn(v, s), s, acc);
+          };
+          upd(lyA, accA);
+          upd(lyB, accB);
+        }
       } else {
-        const float d0 = fmaf(lx, m.da, m.d0);
-        const float dd0 = fmaf(ly0, m.db, d0), dd1 = fmaf(ly1, m.db, d0);
-        const float r0 = rcp_approx(dd0), r1 = rcp_approx(dd1);
-        const float s0 = m.w * r0, s1 = m.w * r1;  // 1/U = SID / depth
-        // depth <= 0: behind the source (projector.hpp:247)
-        if (dd0 > 0.0f) acc0 = fmaf(interp_row(row, a.nb, m.base, nn0 * r0), s0 * s0, acc0);
-        if (dd1 > 0.0f) acc1 = fmaf(interp_row(row, a.nb, m.base, nn1 * r1), s1 * s1, acc1);
+        // checked path: global row, per-pixel behind-source test
+        const float* row = a.sino + (long long)(c0 + k) * a.nb;
+        const float ly[4] = {lyA.x, lyA.y, lyB.x, lyB.y};
+        float add[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float nn = fmaf(ly[q], m.nb, n0);
+          if (!FAN) {
+            add[q] = interp_row(row, a.nb, m.b0, nn);
+          } else {
+            const float dd = fmaf(ly[q], m.db, fmaf(lx, m.da, m.d0));
+            add[q] = 0.0f;
+            if (dd > 0.0f) {  // depth <= 0: behind the source (projector.hpp:247)
+              const float r = rcp_approx(dd);
+              const float sv = sid * r;
+              add[q] = interp_row(row, a.nb, m.b0, nn * r) * sv * sv;
+            }
+          }
+        }
+        accA.x += add[0];
+        accA.y += add[1];
+        accB.x += add[2];
+        accB.y += add[3];
       }
     }
   }
   // cluster reduction: rank r owns pixels p = r, r + G, ... of the tile and
   // sums the G partials in rank order
-  part[ty * kTX + tx] = acc0;
-  part[(ty + 8) * kTX + tx] = acc1;
+  part[ty * kTX + tx] = accA.x;
+  part[(ty + 8) * kTX + tx] = accA.y;
+  part[(ty + 16) * kTX + tx] = accB.x;
+  part[(ty + 24) * kTX + tx] = accB.y;
   cluster.sync();
   for (int p = threadIdx.x; p < kTX * kTY; p += 256) {
     if (p % G != rank) continue;
@@ -465,11 +570,12 @@ void planar_backproject_impl(tg_planar_plan& p, const float* d_sino, float* d_im
   a.sino = d_sino;
   a.img = d_img;
   const dim3 tiles((a.nx + kTX - 1) / kTX, (a.ny + kTY - 1) / kTY, 1);
-  // views split over a cluster of G CTAs per tile: enough CTAs for ~4 waves
-  // at 8 CTAs per SM, at least 8 views per CTA
+  // views split over a cluster of G CTAs per tile: enough CTAs for ~2 waves
+  // at 4 CTAs per SM, at least 16 views per CTA
   const long long nt = (long long)tiles.x * tiles.y;
-  int G = int(std::min<long long>(kMaxCluster, (4LL * p.n_sm * 8 + nt - 1) / nt));
-  G = std::max(1, std::min(G, std::max(1, a.n_views / 8)));
+  int G = int(std::min<long long>(kMaxCluster, (2LL * p.n_sm * 4 + nt - 1) / nt));
+  G = std::max(1, std::min(G, std::max(1, a.n_views / 16)));
+  if (const char* e = std::getenv("TG_PLANAR_G")) G = std::max(1, std::min(kMaxCluster, std::atoi(e)));
   a.vpg = (a.n_views + G - 1) / G;
   KernelTimer timer;
   timer.start(st);

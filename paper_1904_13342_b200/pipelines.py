@@ -33,12 +33,15 @@ def fbp_reconstruct(sino: Sinogram, geo: ParallelGeometry, filt=FilterKind.ramla
     """pipelines.hpp:49-63: BP(filter(p)) * pi / n"""
     if isinstance(filt, FilterKind):
         filt = make_filter(filt, geo.detector.n_bins, geo.detector.spacing)
+    if is_host(sino.data):
+        # host buffers: one upload, K3 + K6 (pi/n fused) on the device, one download
+        data = torch.from_numpy(np.ascontiguousarray(require_f32(sino.data, "sinogram data")))
+        dev_sino = Sinogram(sino.n_projections, detector1d=sino.detector1d, cone=False,
+                            data=data.to(torch.device("cuda", 0)))
+        img = fbp_reconstruct(dev_sino, geo, filt)
+        return Image(geo.volume, img.data.cpu().numpy())
     filtered = apply_filter(sino, filt)
     c = math.pi / float(geo.n_projections)
-    if is_host(filtered.data):
-        img = back_project(filtered, geo)
-        img.data = (img.data.astype(np.float64) * c).astype(np.float32)
-        return img
     return back_project(filtered, geo, scale=c)
 
 
