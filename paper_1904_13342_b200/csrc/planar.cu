@@ -19,6 +19,7 @@
 // through distributed shared memory in a fixed order (deterministic, one
 // writer per pixel, no atomics, no scratch image).
 #include <algorithm>
+#include <cstdlib>
 #include <memory>
 #include <vector>
 
@@ -123,15 +124,19 @@ __device__ __forceinline__ float rcp_approx(float x) {
   return r;
 }
 
-// K5 / K7.  Lane layout: a warp holds 32 / S rays (consecutive bins of a
-// view) x S segments; segment s marches the 64-sample chunks s, s + S, ...
-// of its ray and the segments are summed by a fixed shuffle tree.
+// K5 / K7.  Lane layout: a warp holds 32 adjacent rays (consecutive bins of
+// a view, so its lanes gather neighbouring quads: L1 locality) at one segment;
+// the 8 warps of a CTA hold 8 / S ray groups x S segments, segment s
+// marching the 64-sample chunks s, s + S, ... of its ray.  The segments'
+// partial sums are combined in shared memory by a fixed pairwise tree
+// ((s0 + s1) + (s2 + s3) ...), so the result does not depend on scheduling.
+template <bool REUSE>
 __global__ void __launch_bounds__(256) planar_fp_kernel(const FpArgs a) {
+  __shared__ double part[8][32];
   const int S = a.segs;
-  const int rpw = 32 / S;
-  const int lane = threadIdx.x & 31;
-  const int seg = lane / rpw;
-  const long long ray = (long long)((blockIdx.x * 256 + threadIdx.x) >> 5) * rpw + lane % rpw;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int g = w / S, seg = w % S;
+  const long long ray = ((long long)blockIdx.x * (8 / S) + g) * 32 + lane;
   const long long total_rays = (long long)a.n_views * a.nb;
   double total = 0.0, dt = 0.0;
   bool hit = false;
@@ -172,7 +177,9 @@ __global__ void __launch_bounds__(256) planar_fp_kernel(const FpArgs a) {
           const float tx = __fadd_rd(px, MAGIC), ty = __fadd_rd(py, MAGIC);
           const float wx = px - (tx - MAGIC), wy = py - (ty - MAGIC);
           const int off = (__float_as_int(tx) - MAGIC_BITS) * stx + (__float_as_int(ty) - MAGIC_BITS) * sty;
-          if (off != prev) {
+          if (!REUSE) {
+            q = __ldg(cell + off);  // independent loads: the unrolled loop batches them
+          } else if (off != prev) {
             q = __ldg(cell + off);
             prev = off;
           }
@@ -182,9 +189,17 @@ __global__ void __launch_bounds__(256) planar_fp_kernel(const FpArgs a) {
       }
     }
   }
-  // segments of one ray sit rpw lanes apart: fixed tree, lane seg 0 ends
-  // with the sum over all segments
-  for (int off = rpw; off < 32; off <<= 1) total += __shfl_down_sync(0xffffffffu, total, off);
+  if (S > 1) {
+    part[w][lane] = total;
+    __syncthreads();
+    if (seg == 0) {
+      // pairwise tree over the S segments of this ray group
+      for (int step = 1; step < S; step <<= 1)
+        for (int s0 = 0; s0 + step < S; s0 += 2 * step)
+          part[g * S + s0][lane] += part[g * S + s0 + step][lane];
+      total = part[g * S][lane];
+    }
+  }
   if (seg == 0 && ray < total_rays) a.out[ray] = hit ? float(total * dt) : 0.0f;
 }
 
@@ -516,15 +531,26 @@ void planar_forward_impl(tg_planar_plan& p, const float* d_img, float* d_sino, c
   a.q = p.d_quads;
   a.qT = p.d_quads + nq;
   a.out = d_sino;
-  // threads per ray: enough threads for ~3 waves of 2048 per SM
+  // segments per ray: 4 measured best at both c1 (131k rays) and c2 (369k rays)
+  // (c2: 1 / 2 / 4 / 8 segments 557 / 430 / 389 / 425 us), fewer for long scans
   const long long rays = (long long)a.n_views * a.nb;
-  int S = 1;
-  while (S < 8 && rays * S < 3LL * p.n_sm * 2048) S <<= 1;
+  int S = rays <= 1500000 ? 4 : (rays <= 3000000 ? 2 : 1);
+  if (const char* e = std::getenv("TG_PLANAR_SEGS")) S = std::max(1, std::min(8, std::atoi(e)));
   a.segs = S;
-  const long long warps = (rays + 32 / S - 1) / (32 / S);
+  const long long groups = (rays + 31) / 32;  // 32-ray groups, 8 / S per CTA
   KernelTimer timer;
   timer.start(st);
-  planar_fp_kernel<<<unsigned((warps + 7) / 8), 256, 0, st>>>(a);
+  const unsigned nb = unsigned((groups + 8 / S - 1) / (8 / S));
+  // unconditional gathers (the unrolled loop issues them back to back) beat
+  // skipping a repeated cell by ~2% at c2 (381.6 vs 389.0 us); TG_PLANAR_REUSE=1
+  static const int reuse = [] {
+    const char* e = std::getenv("TG_PLANAR_REUSE");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (reuse)
+    planar_fp_kernel<true><<<nb, 256, 0, st>>>(a);
+  else
+    planar_fp_kernel<false><<<nb, 256, 0, st>>>(a);
   TG_LAUNCHED(1);
   timer.stop();
   p.quads_order.leave(st);
