@@ -291,6 +291,9 @@ def main():
     # (the data path has no collective)
     backend = "nccl" if world <= n_dev else "gloo"
     if world > 1:
+        # NCCL's init log (transport, NVLS / ring choice) goes to stderr
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=dev)
         else:
@@ -405,7 +408,8 @@ def main():
         t1 = time.perf_counter()
         e2e_step()
         e2e_steps_ms.append(1e3 * (time.perf_counter() - t1))
-    e2e_s = max_over_ranks(time.perf_counter() - t0)
+    e2e_own_s = time.perf_counter() - t0
+    e2e_s = max_over_ranks(e2e_own_s)
     e2e_value = updates_total * e2e_n / e2e_s / 1e9
     # the host call back-projects with scale 1; the timed K1 carried the FDK constant
     # bytes actually shipped host -> device per step (each view's own footprint)
@@ -425,6 +429,17 @@ def main():
     d2h_ms = copy_ms(h_slab, slab)
     pcie = {"h2d_gbs": h_band.numel() * 4 / (h2d_ms / 1e3) / 1e9, "h2d_ms": h2d_ms,
             "d2h_gbs": h_slab.numel() * 4 / (d2h_ms / 1e3) / 1e9, "d2h_ms": d2h_ms}
+
+    # ---- per-rank description (N > 1: every rank's shard and times) ---------
+    rank_info = {"rank": rank, "gpu": gpu, "z0": me.z0, "nz": me.nz, "rows": [me.v0, me.n_rows],
+                 "views": [vw0, vwn], "k1_ms": round(k1_avg, 3),
+                 "k1_gups": round(per_gpu_gups, 1), "fp_ms": round(f0.elapsed_time(f1) / args.fp_steps, 3),
+                 "e2e_ms": round(1e3 * e2e_own_s / e2e_n, 3), "h2d_bytes": e2e_h2d // world,
+                 "pcie_h2d_ms": round(h2d_ms, 3), "pcie_h2d_gbs": round(pcie["h2d_gbs"], 1)}
+    ranks = [rank_info]
+    if world > 1:
+        ranks = [None] * world
+        dist.all_gather_object(ranks, rank_info)
 
     # ---- FDK end to end from a full host sinogram (the C++ drop-in's path) ----
     # tg_cone_fdk_host: raw projections [496][960][1248] in pinned host memory ->
@@ -532,6 +547,8 @@ def main():
             "data": "synthetic (SURVEY App. A separable bump, FDK-filtered by K3; Shepp-Logan for FP)",
             "config": bench_config(world),
             "slab": {"z0": me.z0, "nz": me.nz, "rows": [me.v0, me.n_rows]},
+            "ranks": ranks, "backend": backend if world > 1 else None,
+            "nccl_debug": os.environ.get("NCCL_DEBUG"),
             "e2e": {"value": e2e_value, "unit": UNIT,
                     "h2d_bytes_per_step": e2e_h2d,
                     "d2h_bytes_per_step": e2e_d2h,
@@ -595,6 +612,8 @@ def run_c5(tg, D, torch, dist, dev, rank, world, backend, iters, max_over_ranks,
     cfg_name = ("c5: iterative TV cone loop, 1024^3 @0.25mm, 720 x [2048 x 1536] @0.4mm, 360 deg, "
                 f"SID 750 / SDD 1200, lr {C5['lr']}, tv_lambda {C5['tv_lambda']}")
 
+    mode = {"p2p": single_node and world > 1, "fallback": None}
+
     def timed(n_it):
         barrier()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -604,8 +623,12 @@ def run_c5(tg, D, torch, dist, dev, rank, world, backend, iters, max_over_ranks,
                                       tv_lambda=C5["tv_lambda"])
             sino = tg.Sinogram.cone_beam(geo.n_projections, det, data=p)
             _, hist = tg.tv_reconstruct(sino, geo, cfg)
-        elif single_node:
-            _, hist = D.tv_reconstruct_p2p(geo, p, n_it, C5["lr"], C5["tv_lambda"])
+        elif mode["p2p"]:
+            try:
+                _, hist = D.tv_reconstruct_p2p(geo, p, n_it, C5["lr"], C5["tv_lambda"])
+            except D.P2PUnavailable as e:  # raised on every rank together
+                mode["p2p"], mode["fallback"] = False, str(e)[:200]
+                _, hist = D.tv_reconstruct_sharded(geo, p, n_it, C5["lr"], C5["tv_lambda"])
         else:
             _, hist = D.tv_reconstruct_sharded(geo, p, n_it, C5["lr"], C5["tv_lambda"])
         b.record(stream)
@@ -623,8 +646,10 @@ def run_c5(tg, D, torch, dist, dev, rank, world, backend, iters, max_over_ranks,
                                        "GUPS": updates / s_per_it / 1e9},
             "loss_history": hist, "path": "tg_cone_tv_reconstruct" if world == 1 else
             ("distributed.tv_reconstruct_p2p (K8 residual scatter + K9 slab broadcast as "
-             "CUDA-IPC peer stores)" if single_node else
-             "distributed.tv_reconstruct_sharded (NCCL all_to_all + all_gather)")}
+             "CUDA-IPC peer stores)" if mode["p2p"] else
+             "distributed.tv_reconstruct_sharded (NCCL all_to_all + all_gather)"),
+            "p2p_fallback_reason": mode["fallback"],
+            "views_per_rank": vwn}
 
 
 _SAMPLES_CACHE = os.path.join(ROOT, "profiles", "c4_samples.json")

@@ -309,6 +309,11 @@ class PeerBuffers:
         self.own = []
 
 
+class P2PUnavailable(RuntimeError):
+    """Raised on every rank together when the CUDA-IPC peer buffers of
+    tv_reconstruct_p2p cannot be set up on some rank."""
+
+
 def tv_reconstruct_p2p(geo: ConeGeometry, p_part: torch.Tensor, iterations: int,
                        learning_rate: float, tv_lambda: float, group=None,
                        align: int = Z_ALIGN):
@@ -321,8 +326,10 @@ def tv_reconstruct_p2p(geo: ConeGeometry, p_part: torch.Tensor, iterations: int,
     * K9 broadcast (tg_tv_step_multi) stores the updated slab into the next
       volume replica of every rank.
     Replicas are double-buffered (ranks read x_i while peers write x_{i+1});
-    a stream sync + barrier separates the phases.  Bitwise equal to
-    tv_reconstruct_sharded and to the single-GPU loop."""
+    a stream sync + barrier separates the phases: two host barriers per
+    iteration (~0.1 ms each) against ~0.6 s of kernels per iteration per GPU
+    at c5 on 8 GPUs, so device-side peer flags would buy < 0.1%.  Bitwise
+    equal to tv_reconstruct_sharded and to the single-GPU loop."""
     from ._native import Error
     L = N.lib()
     rank, world = dist.get_rank(group), dist.get_world_size(group)
@@ -337,7 +344,22 @@ def tv_reconstruct_p2p(geo: ConeGeometry, p_part: torch.Tensor, iterations: int,
     plane = nx * ny
     vol_bytes = 4 * nx * ny * nz
     band_bytes = 4 * geo.n_projections * me.n_rows * nu
-    bufs = PeerBuffers([band_bytes, vol_bytes, vol_bytes], dix, group)
+    # the peer mappings must succeed on every rank, or no rank uses them: the
+    # decision is collective (MIN of a flag), so every rank raises
+    # P2PUnavailable together and the caller can fall back to the NCCL loop
+    # without a half-entered barrier
+    bufs, why = None, ""
+    try:
+        bufs = PeerBuffers([band_bytes, vol_bytes, vol_bytes], dix, group)
+    except Exception as e:  # reported collectively below
+        why = f"{type(e).__name__}: {e}"
+    ok = torch.tensor([0.0 if bufs is None else 1.0], dtype=torch.float64,
+                      device="cpu" if dist.get_backend(group) == "gloo" else dev)
+    dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=group)
+    if float(ok) < 1.0:
+        if bufs is not None:
+            bufs.close(group)
+        raise P2PUnavailable(why or "a peer rank could not map the CUDA-IPC buffers")
     plan = geo._plan(dix)
     st = torch.cuda.current_stream(dev).cuda_stream
     fp = torch.empty((vwn, nv, nu), dtype=torch.float32, device=dev)
