@@ -130,8 +130,14 @@ __device__ __forceinline__ float rcp_approx(float x) {
 // marching the 64-sample chunks s, s + S, ... of its ray.  The segments'
 // partial sums are combined in shared memory by a fixed pairwise tree
 // ((s0 + s1) + (s2 + s3) ...), so the result does not depend on scheduling.
+// 6 CTAs (48 warps) per SM: the march is L2-latency bound, and a 40-register
+// cap (spills only in the FP64 ray setup) against 64 registers / 4 CTAs:
+// c2 371 -> 320 us, c1 104 -> 99 us (profiles/r2_planar_fp_variants.txt)
+#ifndef TG_PLANAR_FP_MINB
+#define TG_PLANAR_FP_MINB 6
+#endif
 template <bool REUSE>
-__global__ void __launch_bounds__(256) planar_fp_kernel(const FpArgs a) {
+__global__ void __launch_bounds__(256, TG_PLANAR_FP_MINB) planar_fp_kernel(const FpArgs a) {
   __shared__ double part[8][32];
   const int S = a.segs;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -541,11 +547,12 @@ void planar_forward_impl(tg_planar_plan& p, const float* d_img, float* d_sino, c
   KernelTimer timer;
   timer.start(st);
   const unsigned nb = unsigned((groups + 8 / S - 1) / (8 / S));
-  // unconditional gathers (the unrolled loop issues them back to back) beat
-  // skipping a repeated cell by ~2% at c2 (381.6 vs 389.0 us); TG_PLANAR_REUSE=1
+  // re-gather only when the cell changes (at 6 CTAs / SM: c2 320 vs 333 us for
+  // unconditional gathers; at 4 CTAs / SM the unconditional ones won by 2%);
+  // TG_PLANAR_REUSE=0 selects them
   static const int reuse = [] {
     const char* e = std::getenv("TG_PLANAR_REUSE");
-    return e ? std::atoi(e) : 0;
+    return e ? std::atoi(e) : 1;
   }();
   if (reuse)
     planar_fp_kernel<true><<<nb, 256, 0, st>>>(a);
