@@ -346,8 +346,10 @@ __device__ __forceinline__ float interp_row(const float* __restrict__ row, int n
   return lerpf(a0, a1, w);
 }
 
+// 5 CTAs per SM (48 registers; the spills sit in the FP64 map builder and the
+// checked path): c2 93.0 -> 90.3 us against the default 64 registers
 template <bool FAN>
-__global__ void __launch_bounds__(256) planar_bp_kernel(const BpArgs a) {
+__global__ void __launch_bounds__(256, 5) planar_bp_kernel(const BpArgs a) {
   __shared__ ViewMap maps[kChunk];
   __shared__ float rows[kChunk][kRow];
   __shared__ float part[kTX * kTY];
