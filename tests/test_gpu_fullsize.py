@@ -44,20 +44,21 @@ def _bump(seed=0):
 
 def test_c4_fdk_slices_vs_oracle(tg, O, c4):
     """K3 + K1 at full size; oracle back-projection of the identical filtered
-    array on 4 z-slices (top, centre, bottom of the volume)"""
+    array on 64 z-slices: 16 groups of 4 spread from the top to the bottom of
+    the volume (every K1 z-tile position and both tile halves are visited)"""
     raw = _bump()
     filt = tg.fdk_prefilter(raw, c4, True)
     vol = tg.back_project(tg.Sinogram.cone_beam(496, c4.detector, data=filt), c4).data
     f_np = filt.cpu().numpy()
-    for z0 in (0, 254, 508):
-        ref = O.cone_backproject(_oracle_slab(O, c4, z0, 4), f_np)
+    for z0 in np.linspace(0, 508, 16).astype(int):
+        ref = O.cone_backproject(_oracle_slab(O, c4, int(z0), 4), f_np)
         assert_close(vol[z0:z0 + 4].cpu().numpy(), ref, what=f"c4 BP slices {z0}")
 
 
 def test_c4_prefilter_rows_vs_oracle(tg, O, c4):
     raw = _bump()
     filt = tg.fdk_prefilter(raw, c4, True).cpu().numpy()
-    views = [0, 137, 495]
+    views = [0, 62, 137, 186, 248, 310, 401, 495]
     s = raw[views].cpu().numpy()
     og = _oracle_slab(O, c4, 0, 1)
     w = O.apply_weights(s, O.cosine_weights_cone(og))
@@ -70,14 +71,22 @@ def test_c4_prefilter_rows_vs_oracle(tg, O, c4):
 
 
 def test_c4_forward_views_vs_oracle(tg, O, c4):
-    """K2 at full size: two views against the oracle, exact zero pattern"""
+    """K2 at full size: eight views spread over the 220 deg scan against the
+    oracle, exact zero pattern, through both K2 kernels (quad volume: the one
+    the autotune keeps at c4; slab-staged), which give identical bits"""
     ph = tg.shepp_logan_3d(c4.volume, device=DEV).data
-    views = [3, 301]
+    views = [3, 65, 130, 190, 250, 301, 370, 490]
     og = O.cone_from_matrices(O.make_volume([512] * 3, [0.5] * 3),
                               O.det2_centered(1248, 960, 0.64, 0.64), c4.angular_range, c4.sid,
                               c4.sdd, c4.matrices[views])
     ref = O.cone_forward(og, ph.cpu().numpy())
-    out = torch.stack([tg.cone_forward_views(c4, ph, v, 1)[0] for v in views]).cpu().numpy()
+    outs = {}
+    for impl in (0, 1):
+        tg.set_cone_knob(c4, "k2_impl", impl)
+        outs[impl] = torch.stack([tg.cone_forward_views(c4, ph, v, 1)[0] for v in views]).cpu().numpy()
+    tg.set_cone_knob(c4, "k2_impl", -1)
+    out = outs[1]
+    assert np.array_equal(outs[0], outs[1])
     assert_close(out, ref, what="c4 FP views")
     assert np.array_equal(out == 0.0, ref == 0.0)
 
