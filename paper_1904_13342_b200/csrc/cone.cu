@@ -364,7 +364,7 @@ __global__ void __maxnreg__(CIRC ? 72 : 96)
         // MUFU reciprocal (~1 ulp; no IEEE slow path in the per-view prologue)
         float r;
         asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(hz0));
-        const float invw2 = a.sid2 * r * r;
+        const float invw2 = r * r;  // SID^2 is applied in the epilogue
         const float u = un * r;
         const float fu = floorf(u);
         const float wu = u - fu;
@@ -425,31 +425,33 @@ __global__ void __maxnreg__(CIRC ? 72 : 96)
         }
       } else {
         // general calibrated matrices: the full projective map per voxel,
-        // voxels k and k + K/2 as FP32x2 pairs; the reciprocal is the MUFU
-        // approximation (~1 ulp: far inside the parity tolerance), the
-        // address takes the run-time magic bias like the circular path
+        // voxels k and k + K/2 as FP32x2 pairs.  Along a column the depth hz and
+        // the u / v numerators are affine in k, so each is one FFMA2 from
+        // per-view bases; the reciprocal is the MUFU approximation (~1 ulp: far
+        // inside the parity tolerance); 1/w^2 = SID^2 r^2 with SID^2 folded into
+        // the epilogue's scale (every mode accumulates r^2-weighted taps); full
+        // tiles use compile-time voxel offsets (no clamp)
         constexpr int H = K / 2;
         const uint32_t base2 = sbase + a.magic_row_off + 0u - MAGIC_BITS * 4u;
-        const float2 sz2 = make_float2(sz, sz), dz02 = make_float2(dz0, dz0);
-        const float2 Wz = make_float2(W.z, W.z), Uz = make_float2(U.z, U.z), Vz = make_float2(V.z, V.z);
-        const float2 hz02 = make_float2(hz0, hz0), un2 = make_float2(un, un), vn2 = make_float2(vn, vn);
-        const float2 sid22 = make_float2(a.sid2, a.sid2);
+        const float hzA = fmaf(W.z, dz0, hz0), hzS = W.z * sz;
+        const float nuA = fmaf(U.z, dz0, un), nuS = U.z * sz;
+        const float nvA = fmaf(V.z, dz0, vn), nvS = V.z * sz;
+        const float2 hzA2 = make_float2(hzA, hzA), hzS2 = make_float2(hzS, hzS);
+        const float2 nuA2 = make_float2(nuA, nuA), nuS2 = make_float2(nuS, nuS);
+        const float2 nvA2 = make_float2(nvA, nvA), nvS2 = make_float2(nvS, nvS);
         const float2 M2 = make_float2(MAGIC, MAGIC), nM2 = make_float2(-MAGIC, -MAGIC);
-#pragma unroll
-        for (int k = 0; k < H; ++k) {
-          const float2 kk = make_float2(float(min(k, kmax)), float(min(k + H, kmax)));
-          const float2 dz = __ffma2_rn(kk, sz2, dz02);
-          const float2 hz = __ffma2_rn(Wz, dz, hz02);
+        auto voxel_pair = [&](float2 kk, float2& acc2) {
+          const float2 hz = __ffma2_rn(kk, hzS2, hzA2);
           float2 r;
           asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r.x) : "f"(hz.x));
           asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r.y) : "f"(hz.y));
-          const float2 u = __fmul2_rn(__ffma2_rn(Uz, dz, un2), r);
-          const float2 v = __fmul2_rn(__ffma2_rn(Vz, dz, vn2), r);
+          const float2 u = __fmul2_rn(__ffma2_rn(kk, nuS2, nuA2), r);
+          const float2 v = __fmul2_rn(__ffma2_rn(kk, nvS2, nvA2), r);
           const float2 tu = __fadd2_rd(u, M2), tv = __fadd2_rd(v, M2);
           const float2 fu = __fadd2_rn(tu, nM2), fv = __fadd2_rn(tv, nM2);
           const float2 wu = __fadd2_rn(u, make_float2(-fu.x, -fu.y));
           const float2 wv = __fadd2_rn(v, make_float2(-fv.x, -fv.y));
-          const float2 iw = __fmul2_rn(__fmul2_rn(sid22, r), r);
+          const float2 iw = __fmul2_rn(r, r);
           float a0, a1, b0, b1, c0, c1, d0, d1;
           lds_quad<ROWB>(mad_u32<ROWB>(__float_as_uint(tv.x), base2 + __float_as_uint(tu.x) * 4u),
                          a0, a1, b0, b1);
@@ -460,7 +462,15 @@ __global__ void __maxnreg__(CIRC ? 72 : 96)
           const float2 top = __ffma2_rn(wu, __fadd2_rn(p1, make_float2(-p0.x, -p0.y)), p0);
           const float2 bot = __ffma2_rn(wu, __fadd2_rn(q1, make_float2(-q0.x, -q0.y)), q0);
           const float2 mid = __ffma2_rn(wv, __fadd2_rn(bot, make_float2(-top.x, -top.y)), top);
-          acc[k] = __ffma2_rn(mid, iw, acc[k]);
+          acc2 = __ffma2_rn(mid, iw, acc2);
+        };
+        if (kmax == K - 1) {
+#pragma unroll
+          for (int k = 0; k < H; ++k) voxel_pair(make_float2(float(k), float(k + H)), acc[k]);
+        } else {
+#pragma unroll
+          for (int k = 0; k < H; ++k)
+            voxel_pair(make_float2(float(min(k, kmax)), float(min(k + H, kmax))), acc[k]);
         }
       }
     } else if (mode == MODE_SLOW) {
@@ -473,7 +483,7 @@ __global__ void __maxnreg__(CIRC ? 72 : 96)
         if (!(hz > 0.0f)) continue;  // behind the source (projector.hpp:302)
         const float u = fmaf(U.z, dz, un) / hz, v = fmaf(V.z, dz, vn) / hz;
         if (!(fabsf(u) < 4.0e6f) || !(fabsf(v) < 4.0e6f)) continue;
-        ACC(k) += bilinear_global(a, img, u, v) * (a.sid2 / (hz * hz));
+        ACC(k) += bilinear_global(a, img, u, v) * (1.0f / (hz * hz));  // SID^2 in the epilogue
       }
     }
     __syncwarp();
@@ -482,11 +492,12 @@ __global__ void __maxnreg__(CIRC ? 72 : 96)
 
   // the previous grid of the stream (PDL) has finished writing the volume
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  // the taps were weighted by 1/hz^2; 1/w^2 = SID^2 / hz^2 (projector.hpp:306)
+  const float sc = a.scale * a.sid2;
   float4 v4[K / 4];
 #pragma unroll
   for (int b = 0; b < K / 4; ++b)
-    v4[b] = make_float4(ACC(4 * b) * a.scale, ACC(4 * b + 1) * a.scale, ACC(4 * b + 2) * a.scale,
-                        ACC(4 * b + 3) * a.scale);
+    v4[b] = make_float4(ACC(4 * b) * sc, ACC(4 * b + 1) * sc, ACC(4 * b + 2) * sc, ACC(4 * b + 3) * sc);
   k1_store<K / 4>(a, v4, lane, tile.x0 + (lx & ~3), gy, tile.z0, kmax);
 }
 
