@@ -191,6 +191,12 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   }
 }
 
+// For a producer warp that runs ahead of its consumers: back off between
+// polls so the spin does not take issue slots from the consumer warps.
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity, unsigned ns) {
+  while (!mbar_try_wait(bar, parity)) __nanosleep(ns);
+}
+
 // TMA: 3D tile load global -> shared, completion counted on `bar` (bytes).
 // Out-of-bounds elements (including negative coordinates) are zero-filled,
 // which is exactly the reference's zero-padded interpolation
