@@ -1749,7 +1749,7 @@ void phased_backproject(tg_cone_plan& p, uint64_t z0, uint64_t nz, uint64_t v0, 
   const uint64_t lo_u = (units - centre) / 2, hi_u = lo_u + centre;
   phases.push_back({slices(lo_u, hi_u)});
   const uint64_t below = lo_u, above = units - hi_u;
-  const int kRings = knob("TG_E2E_RINGS", 2);
+  const int kRings = knob("TG_E2E_RINGS", 3);
   for (int r = 0; r < kRings; ++r) {
     const uint64_t b0 = below * r / kRings, b1 = below * (r + 1) / kRings;
     const uint64_t a0 = above * r / kRings, a1 = above * (r + 1) / kRings;

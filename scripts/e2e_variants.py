@@ -57,7 +57,19 @@ def sweep():
     # and with it more chunks (whose launch tails PDL now hides)
     # (measured: 2/2/4 43.3 ms with PDL, 44.2 without; 8 chunks 45.7; 2/4/4 43.7;
     # 2/3/6 44.8; 1/2/4 44.8 — profiles/r1_e2e_pdl_sweep.jsonl)
-    for c, r, ch, g, mode in [("2", "2", "4", "8", "pdl"), ("2", "2", "4", "8", "nopdl")]:
+    # round 2 (K1 36.5 ms after the 4-view producer): re-sweep around 2/2/4
+    grid = [("2", "2", "4", "8", "pdl"), ("1", "2", "4", "8", "pdl"), ("2", "2", "3", "8", "pdl"),
+            ("2", "2", "6", "8", "pdl"), ("2", "3", "4", "8", "pdl"), ("1", "3", "4", "8", "pdl"),
+            ("2", "2", "4", "4", "pdl"), ("2", "2", "4", "16", "pdl"), ("1", "2", "3", "8", "pdl")]
+    # measured: 2/2/4/8 40.92, 2/3/4/8 40.33, 2/2/4/16 40.64, 1/3/4/8 40.99, 2/2/3/8 41.25,
+    # 2/2/6/8 42.76 ms (profiles/r2_e2e_sweep.jsonl)
+    if "--grid2" in sys.argv:
+        grid = [("2", "3", "4", "8", "pdl"), ("2", "3", "4", "16", "pdl"), ("2", "4", "4", "8", "pdl"),
+                ("2", "4", "4", "16", "pdl"), ("3", "3", "4", "8", "pdl"), ("2", "3", "5", "8", "pdl"),
+                ("2", "3", "4", "12", "pdl"), ("2", "5", "4", "8", "pdl")]
+    if "--grid1" in sys.argv:
+        grid = [("2", "2", "4", "8", "pdl"), ("2", "2", "4", "8", "nopdl")]
+    for c, r, ch, g, mode in grid:
         env = dict(os.environ, TG_E2E_CENTRE_UNITS=c, TG_E2E_RINGS=r, TG_E2E_CHUNKS=ch,
                    TG_E2E_GROUP=g)
         if mode == "nopdl":
