@@ -181,6 +181,7 @@ __device__ __forceinline__ void march(const Args& a, Ray& r, const RayRef& rs, i
   const int P = __reduce_max_sync(0xffffffffu, pairs);
   uint32_t cbase = chunk_base<WH, XDOM>(r, sbase, od, hb, d0, zb);
   float sum = r.sum;
+#pragma unroll 2
   for (int p = 0; p < P; ++p) {
     if (p < pairs) {
       if (r.k - r.k0 == 64) {
