@@ -377,7 +377,6 @@ __global__ void __launch_bounds__(NTHREADS, 2)
     if (lane == 0 && axis == 1) prefetch_tensor_map(&tmapY);
     for (int i = 0; i < n_slabs; ++i) {
       const int s = i % a.stages;
-      if (i >= a.stages) mbar_wait(&empty[s], ((i / a.stages) - 1) & 1);
       StageHdr h;
       h.mode = MODE_GLOBAL;
       h.hb = h.zb = 0;
@@ -419,6 +418,9 @@ __global__ void __launch_bounds__(NTHREADS, 2)
           if (wneed <= WH && zneed <= a.boxZ) h.mode = MODE_SMEM;
         }
       }
+      // the box is computed before the stage frees up: only the header write and
+      // the TMA issue wait for the consumers
+      if (i >= a.stages) mbar_wait(&empty[s], ((i / a.stages) - 1) & 1);
       if (lane == 0) {
         hdr[s] = h;
         if (a.stats) {
