@@ -1449,7 +1449,12 @@ void k2_autotune(tg_cone_plan& p, const float* d_vol, cudaStream_t st) {
   cudaEventDestroy(a);
   cudaEventDestroy(b);
   TG_CUDA(cudaFree(scratch));
-  p.k2_impl = (ms[0] < 0.97f * ms[1]) ? 0 : 1;
+  // the faster one; slab on near-ties (within 3%) only when the quad volumes
+  // are a large share of the device (8.8x the volume against the slab's 2x).
+  // Short view blocks understate the quad kernel's lead at c4 (4% sampled,
+  // 9% over a whole scan), so the tie band must not cover that case.
+  const bool big = 2 * one > total_b / 8;
+  p.k2_impl = (ms[0] < (big ? 0.97f : 1.0f) * ms[1]) ? 0 : 1;
   // drop the loser's scratch (the stream is idle: synchronised above)
   if (p.k2_impl == 1 && p.d_vpad) {
     TG_CUDA(cudaFree(p.d_vpad));
