@@ -1745,16 +1745,18 @@ void phased_backproject(tg_cone_plan& p, uint64_t z0, uint64_t nz, uint64_t v0, 
     return Range{a, b > a ? b - a : 0};
   };
   std::vector<std::vector<Range>> phases;
-  // schedule knobs (experiments; defaults measured best at c4)
+  // schedule knobs (experiments; defaults measured best at c4, round 2: the BP
+  // path 2 / 3 / 4 (profiles/r2_e2e_sweep.jsonl), the FDK path — PCIe-bound
+  // with whole detector rows — 1 / 5 / 3 (profiles/r2_e2e_fdk_sweep.jsonl))
   auto knob = [](const char* name, int dflt) {
     const char* e = std::getenv(name);
     return e ? std::max(1, std::atoi(e)) : dflt;
   };
-  const uint64_t centre = std::min<uint64_t>(units, uint64_t(knob("TG_E2E_CENTRE_UNITS", 2)));
+  const uint64_t centre = std::min<uint64_t>(units, uint64_t(knob("TG_E2E_CENTRE_UNITS", fdk ? 1 : 2)));
   const uint64_t lo_u = (units - centre) / 2, hi_u = lo_u + centre;
   phases.push_back({slices(lo_u, hi_u)});
   const uint64_t below = lo_u, above = units - hi_u;
-  const int kRings = knob("TG_E2E_RINGS", 3);
+  const int kRings = knob("TG_E2E_RINGS", fdk ? 5 : 3);
   for (int r = 0; r < kRings; ++r) {
     const uint64_t b0 = below * r / kRings, b1 = below * (r + 1) / kRings;
     const uint64_t a0 = above * r / kRings, a1 = above * (r + 1) / kRings;
@@ -1763,7 +1765,7 @@ void phased_backproject(tg_cone_plan& p, uint64_t z0, uint64_t nz, uint64_t v0, 
     if (a1 > a0) ph.push_back(slices(hi_u + a0, hi_u + a1));
     if (!ph.empty()) phases.push_back(ph);
   }
-  const int kChunks = knob("TG_E2E_CHUNKS", 4);
+  const int kChunks = knob("TG_E2E_CHUNKS", fdk ? 3 : 4);
   const int kGroup = knob("TG_E2E_GROUP", 8);
   // view chunks are whole copy groups (a group's residency is tracked for all
   // of its views at once)

@@ -28,10 +28,19 @@ def one():
     h_slab = torch.empty((me.nz, 512, 512), dtype=torch.float32, pin_memory=True)
     L = tg._native.lib()
     plan = geo._plan(0)
+    if os.environ.get("E2E_FDK"):
+        # the FDK from a full host sinogram (tg_cone_fdk_host, bench.py's fdk_e2e leg)
+        h_sino = torch.zeros((bench.C4["views"], bench.C4["nv"], bench.C4["nu"]), dtype=torch.float32,
+                             pin_memory=True)
+        h_sino[:, me.v0:me.v0 + me.n_rows].copy_(band.cpu())
+        h_vol = torch.empty((512, 512, 512), dtype=torch.float32, pin_memory=True)
 
-    def step():
-        tg._native.check(L.tg_cone_backproject_slab_host(plan, me.z0, me.nz, me.v0, me.n_rows,
-                                                         h_band.data_ptr(), h_slab.data_ptr(), 0, 1))
+        def step():
+            tg._native.check(L.tg_cone_fdk_host(plan, h_sino.data_ptr(), h_vol.data_ptr(), 1))
+    else:
+        def step():
+            tg._native.check(L.tg_cone_backproject_slab_host(plan, me.z0, me.nz, me.v0, me.n_rows,
+                                                             h_band.data_ptr(), h_slab.data_ptr(), 0, 1))
     for _ in range(2):
         step()
     ts = []
@@ -42,7 +51,7 @@ def one():
     ms = 1e3 * sorted(ts)[len(ts) // 2]
     print(json.dumps({k: os.environ.get(k, "default") for k in
                       ("TG_E2E_CENTRE_UNITS", "TG_E2E_RINGS", "TG_E2E_CHUNKS", "TG_E2E_GROUP",
-                               "TG_E2E_NOPDL")} |
+                               "TG_E2E_NOPDL", "E2E_FDK")} |
                      {"h2d_bytes": int(L.tg_cone_last_h2d_bytes(plan))} |
                      {"ms_med": ms, "ms_min": 1e3 * min(ts),
                       "gups": 512 ** 3 * 496 / (ms / 1e3) / 1e9}), flush=True)
@@ -63,6 +72,15 @@ def sweep():
             ("2", "2", "4", "4", "pdl"), ("2", "2", "4", "16", "pdl"), ("1", "2", "3", "8", "pdl")]
     # measured: 2/2/4/8 40.92, 2/3/4/8 40.33, 2/2/4/16 40.64, 1/3/4/8 40.99, 2/2/3/8 41.25,
     # 2/2/6/8 42.76 ms (profiles/r2_e2e_sweep.jsonl)
+    if "--fdk" in sys.argv:
+        os.environ["E2E_FDK"] = "1"
+        grid = [(c, r, ch, "8", "pdl") for c in ("1", "2") for r in ("2", "3", "4")
+                for ch in ("3", "4", "6")]
+        # measured (profiles/r2_e2e_fdk_sweep.jsonl): 1/4/3 46.05 ms, 2/3/4 46.46, 2/2/4 47.54
+        if "--fdk2" in sys.argv:
+            grid = [("1", r, ch, g, "pdl") for r, ch, g in (("4", "3", "8"), ("5", "3", "8"),
+                    ("6", "3", "8"), ("5", "2", "8"), ("4", "2", "8"), ("5", "3", "16"),
+                    ("8", "3", "8"), ("6", "2", "8"))]
     if "--grid2" in sys.argv:
         grid = [("2", "3", "4", "8", "pdl"), ("2", "3", "4", "16", "pdl"), ("2", "4", "4", "8", "pdl"),
                 ("2", "4", "4", "16", "pdl"), ("3", "3", "4", "8", "pdl"), ("2", "3", "5", "8", "pdl"),
