@@ -605,11 +605,10 @@ void planar_backproject_impl(tg_planar_plan& p, const float* d_sino, float* d_im
   a.sino = d_sino;
   a.img = d_img;
   const dim3 tiles((a.nx + kTX - 1) / kTX, (a.ny + kTY - 1) / kTY, 1);
-  // views split over a cluster of G CTAs per tile: enough CTAs for ~2 waves
-  // at 4 CTAs per SM, at least 16 views per CTA
-  const long long nt = (long long)tiles.x * tiles.y;
-  int G = int(std::min<long long>(kMaxCluster, (2LL * p.n_sm * 4 + nt - 1) / nt));
-  G = std::max(1, std::min(G, std::max(1, a.n_views / 16)));
+  // views split over a cluster of G CTAs per tile, at least 16 views per CTA:
+  // 8 measured best at c1 (64 tiles) and c2 (256 tiles) — c2 4 / 5 / 8 / 12 /
+  // 16: 89.9 / 90.3 / 88.3 / 108 / 125 us (12 and 16 need non-portable clusters)
+  int G = std::max(1, std::min(kMaxCluster, a.n_views / 16));
   if (const char* e = std::getenv("TG_PLANAR_G")) G = std::max(1, std::min(kMaxCluster, std::atoi(e)));
   a.vpg = (a.n_views + G - 1) / G;
   KernelTimer timer;
