@@ -228,6 +228,14 @@ __device__ __noinline__ void k1_store(const BpArgs& a, const float4* v4, int lan
 
 // producer back-off between empty-barrier polls (c4 K1: 37.24 ms spinning,
 // 37.12 / 36.83 / 36.63 / 36.51 / 36.59 ms at 32 / 128 / 512 / 2048 / 4096 ns)
+#ifndef TG_K1_GEN_FMARM
+#define TG_K1_GEN_FMARM 1
+#endif
+
+#ifndef TG_K1_GEN_PIPE
+#define TG_K1_GEN_PIPE 1
+#endif
+
 #ifndef TG_K1_BACKOFF_NS
 #define TG_K1_BACKOFF_NS 2048
 #endif
@@ -478,9 +486,64 @@ __global__ void __maxnreg__(CIRC ? 72 : 96)
           const float2 mid = __ffma2_rn(wv, __fadd2_rn(bot, make_float2(-top.x, -top.y)), top);
           acc2 = __ffma2_rn(mid, iw, acc2);
         };
+        struct GTaps {
+          float a0, a1, b0, b1, c0, c1, d0, d1;
+          float2 wu, wv, iw;
+        };
+        auto gfetch = [&](float2 kk, GTaps& q) {
+          const float2 hz = __ffma2_rn(kk, hzS2, hzA2);
+          float2 r;
+          asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r.x) : "f"(hz.x));
+          asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r.y) : "f"(hz.y));
+          const float2 nu = __ffma2_rn(kk, nuS2, nuA2), nv = __ffma2_rn(kk, nvS2, nvA2);
+#if TG_K1_GEN_FMARM
+          // floor of the exact product nu * r: t = RD(nu * r + M) in one FFMA
+          // (round-down magic), the fraction as one FFMA against the floor.  It
+          // can differ from floor(RN(nu * r)) only when the product lies within
+          // half an ulp below an integer n: then the taps are (n - 1, n) with
+          // weight RN(nu * r - (n - 1)) = 1 — the same bilinear value, and inside
+          // the box's one-pixel margin (make_footprint)
+          const float2 tu = __ffma2_rd(nu, r, M2), tv = __ffma2_rd(nv, r, M2);
+          const float2 fu = __fadd2_rn(tu, nM2), fv = __fadd2_rn(tv, nM2);
+          q.wu = __ffma2_rn(nu, r, make_float2(-fu.x, -fu.y));
+          q.wv = __ffma2_rn(nv, r, make_float2(-fv.x, -fv.y));
+#else
+          const float2 u = __fmul2_rn(nu, r);
+          const float2 v = __fmul2_rn(nv, r);
+          const float2 tu = __fadd2_rd(u, M2), tv = __fadd2_rd(v, M2);
+          const float2 fu = __fadd2_rn(tu, nM2), fv = __fadd2_rn(tv, nM2);
+          q.wu = __fadd2_rn(u, make_float2(-fu.x, -fu.y));
+          q.wv = __fadd2_rn(v, make_float2(-fv.x, -fv.y));
+#endif
+          q.iw = __fmul2_rn(r, r);
+          lds_quad_v<ROWB>(mad_u32<ROWB>(__float_as_uint(tv.x), base2 + __float_as_uint(tu.x) * 4u),
+                           q.a0, q.a1, q.b0, q.b1);
+          lds_quad_v<ROWB>(mad_u32<ROWB>(__float_as_uint(tv.y), base2 + __float_as_uint(tu.y) * 4u),
+                           q.c0, q.c1, q.d0, q.d1);
+        };
+        auto gblend = [&](const GTaps& q, float2& acc2) {
+          const float2 p0 = make_float2(q.a0, q.c0), p1 = make_float2(q.a1, q.c1);
+          const float2 q0 = make_float2(q.b0, q.d0), q1 = make_float2(q.b1, q.d1);
+          const float2 top = __ffma2_rn(q.wu, __fadd2_rn(p1, make_float2(-p0.x, -p0.y)), p0);
+          const float2 bot = __ffma2_rn(q.wu, __fadd2_rn(q1, make_float2(-q0.x, -q0.y)), q0);
+          const float2 mid = __ffma2_rn(q.wv, __fadd2_rn(bot, make_float2(-top.x, -top.y)), top);
+          acc2 = __ffma2_rn(mid, q.iw, acc2);
+        };
         if (kmax == K - 1) {
+#if TG_K1_GEN_PIPE
+          // software pipeline as in the circular path: pair k+1's map and
+          // loads are issued before pair k's lerps
+          GTaps gq[2];
+          gfetch(make_float2(0.f, float(H)), gq[0]);
+#pragma unroll
+          for (int k = 0; k < H; ++k) {
+            if (k + 1 < H) gfetch(make_float2(float(k + 1), float(k + 1 + H)), gq[(k + 1) & 1]);
+            gblend(gq[k & 1], acc[k]);
+          }
+#else
 #pragma unroll
           for (int k = 0; k < H; ++k) voxel_pair(make_float2(float(k), float(k + H)), acc[k]);
+#endif
         } else {
 #pragma unroll
           for (int k = 0; k < H; ++k)
