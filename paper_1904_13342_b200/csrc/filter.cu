@@ -201,12 +201,9 @@ void destroy(RowFilter* f) {
 }
 
 // FDK pre-weights as one elementwise pass: one warp per detector row (no
-// per-element index division; 8 rows per CTA), float4 loads / stores when
-// rows are 16-byte aligned, each lane keeping two float4 in flight; the FP64
+// per-element index division; 8 rows per CTA); the FP64
 // products and their two fp32 roundings are the reference's
-// (filtering.hpp:136-154, applied cosine then Parker).  One CTA of 256
-// threads per 312-float4 row left 56 threads with a second round: 1.2 ms at
-// c4's band.
+// (filtering.hpp:136-154, applied cosine then Parker).
 constexpr int kPwRows = 8;
 __global__ void __launch_bounds__(32 * kPwRows) preweight_kernel(const float* in, float* out, int n,
                                                                  uint64_t n_rows, PreWeights pw,
@@ -227,28 +224,20 @@ __global__ void __launch_bounds__(32 * kPwRows) preweight_kernel(const float* in
     if (pk) v = float(double(v) * __ldg(pk + j));
     return v;
   };
-  auto weigh4 = [&](float4 v, int j) {
-    v.x = weigh(v.x, j);
-    v.y = weigh(v.y, j + 1);
-    v.z = weigh(v.z, j + 2);
-    v.w = weigh(v.w, j + 3);
-    return v;
-  };
-  if ((n & 3) == 0 && (reinterpret_cast<uintptr_t>(src) & 15) == 0 &&
-      (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
-    const float4* s4 = reinterpret_cast<const float4*>(src);
-    float4* d4 = reinterpret_cast<float4*>(dst);
-    const int n4 = n / 4;
-    int c = lane;
-    for (; c + 32 < n4; c += 64) {
-      const float4 a = __ldcs(s4 + c), b = __ldcs(s4 + c + 32);
-      __stcs(d4 + c, weigh4(a, 4 * c));
-      __stcs(d4 + c + 32, weigh4(b, 4 * (c + 32)));
-    }
-    if (c < n4) __stcs(d4 + c, weigh4(__ldcs(s4 + c), 4 * c));
-  } else {
-    for (int j = lane; j < n; j += 32) dst[j] = weigh(src[j], j);
+  // lane j of every 32: the FP64 weight rows are read as 256-byte warp
+  // segments (2 L1 wavefronts per 32 elements; per-lane float4 with 32-byte
+  // lane strides cost 8 per instruction: 4.35 -> 4.23 ms for K3 at c4), four
+  // elements in flight per lane
+  int j = lane;
+  for (; j + 96 < n; j += 128) {
+    const float a0 = __ldcs(src + j), a1 = __ldcs(src + j + 32), a2 = __ldcs(src + j + 64),
+                a3 = __ldcs(src + j + 96);
+    __stcs(dst + j, weigh(a0, j));
+    __stcs(dst + j + 32, weigh(a1, j + 32));
+    __stcs(dst + j + 64, weigh(a2, j + 64));
+    __stcs(dst + j + 96, weigh(a3, j + 96));
   }
+  for (; j < n; j += 32) __stcs(dst + j, weigh(__ldcs(src + j), j));
 }
 
 void apply(const RowFilter& f, const float* d_in, float* d_out, uint64_t n_rows,
