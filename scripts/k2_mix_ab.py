@@ -1,4 +1,7 @@
-"""K2 quad kernel with slice z+1 gathered by tld4 from a layered texture
+"""[Experiment record: the TG_K2_MIX variant was removed after this
+measurement, profiles/r2_k2_bank_model.txt; without it both runs time the
+plain quad kernel.]
+K2 quad kernel with slice z+1 gathered by tld4 from a layered texture
 (TG_K2_MIX=1) against the plain quad kernel (two LDG.128 per sample), forced
 k2_impl 0, at c4 (all 496 views) and c5 (views 0-89); bitwise comparison."""
 import json
