@@ -1834,6 +1834,16 @@ void phased_backproject(tg_cone_plan& p, uint64_t z0, uint64_t nz, uint64_t v0, 
   // of its views at once)
   const uint64_t chunk = ((np + kChunks - 1) / kChunks + kGroup - 1) / kGroup * kGroup;
   const int n_chunks = int((np + chunk - 1) / chunk);
+  // BP: phases from the third on run in fewer, larger view chunks — the copy
+  // engine is ahead of K1 by then, and the 32 K1 launches of the uniform
+  // schedule cost 40.2 ms serialised against 36.5 for one launch (launch
+  // tails).  c4: 40.27 -> 39.42 ms with 2 chunks from phase 2 (1 chunk 45.1,
+  // from phase 1 41.5; scripts/e2e_variants.py --late / --late2,
+  // profiles/r2_e2e_late_sweep.jsonl)
+  const int kChunksLate = fdk ? kChunks : knob("TG_E2E_CHUNKS_LATE", 2);
+  const int kLateFrom = knob("TG_E2E_LATE_FROM", 2);
+  const uint64_t chunk_late = ((np + kChunksLate - 1) / kChunksLate + kGroup - 1) / kGroup * kGroup;
+  const int n_chunks_late = int((np + chunk_late - 1) / chunk_late);
   const int n_phases = int(phases.size());
   // consecutive K1 launches overlap (programmatic dependent launch); never a
   // K1 right after the K3 that produces its rows (FDK)
@@ -1910,7 +1920,7 @@ void phased_backproject(tg_cone_plan& p, uint64_t z0, uint64_t nz, uint64_t v0, 
     g_ub[gi] = fdk ? int64_t(nu) : std::min<int64_t>(int64_t(nu), (g_ub[gi] + 15) / 16 * 16);
   }
 
-  HostPipe& hp = plan_pipe(p, n_phases * n_chunks + n_phases + int(units) + 1);
+  HostPipe& hp = plan_pipe(p, n_phases * std::max(n_chunks, n_chunks_late) + n_phases + int(units) + 1);
   cudaStream_t ds = hp.ds;  // downloads: concurrent with the uploads on xs
   int ev = 0;
   uint64_t shipped = 0;
@@ -1942,8 +1952,10 @@ void phased_backproject(tg_cone_plan& p, uint64_t z0, uint64_t nz, uint64_t v0, 
   for (int ph = 0; ph < n_phases; ++ph) {
     // slices of this phase (its ranges are contiguous below / above the centre)
     const bool last = ph == n_phases - 1;
-    for (int c = 0; c < n_chunks; ++c) {
-      const uint64_t w0 = uint64_t(c) * chunk, wn = std::min(chunk, np - w0);
+    const uint64_t ch_ph = ph >= kLateFrom ? chunk_late : chunk;
+    const int nch_ph = ph >= kLateFrom ? n_chunks_late : n_chunks;
+    for (int c = 0; c < nch_ph; ++c) {
+      const uint64_t w0 = uint64_t(c) * ch_ph, wn = std::min(ch_ph, np - w0);
       for (uint64_t gi = w0 / G; gi * G < w0 + wn; ++gi) {
         const uint64_t a = std::max<uint64_t>(gi * G, w0);
         const uint64_t b = std::min<uint64_t>((gi + 1) * G, w0 + wn);
@@ -1988,7 +2000,7 @@ void phased_backproject(tg_cone_plan& p, uint64_t z0, uint64_t nz, uint64_t v0, 
       // chunk's first K1 follows the K3 that filtered its rows
       bool after_k3 = fdk && filtered;
       fresh.clear();
-      if (last && c == n_chunks - 1) {
+      if (last && c == nch_ph - 1) {
         for (const Range& r : phases[ph])
           for (uint64_t q = 0; q < r.n; q += 32) {
             const Range part{r.z + q, std::min<uint64_t>(32, r.n - q)};

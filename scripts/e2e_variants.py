@@ -51,7 +51,7 @@ def one():
     ms = 1e3 * sorted(ts)[len(ts) // 2]
     print(json.dumps({k: os.environ.get(k, "default") for k in
                       ("TG_E2E_CENTRE_UNITS", "TG_E2E_RINGS", "TG_E2E_CHUNKS", "TG_E2E_GROUP",
-                               "TG_E2E_NOPDL", "E2E_FDK")} |
+                               "TG_E2E_NOPDL", "E2E_FDK", "TG_E2E_CHUNKS_LATE", "TG_E2E_LATE_FROM")} |
                      {"h2d_bytes": int(L.tg_cone_last_h2d_bytes(plan))} |
                      {"ms_med": ms, "ms_min": 1e3 * min(ts),
                       "gups": 512 ** 3 * 496 / (ms / 1e3) / 1e9}), flush=True)
@@ -85,6 +85,16 @@ def sweep():
         grid = [("2", "3", "4", "8", "pdl"), ("2", "3", "4", "16", "pdl"), ("2", "4", "4", "8", "pdl"),
                 ("2", "4", "4", "16", "pdl"), ("3", "3", "4", "8", "pdl"), ("2", "3", "5", "8", "pdl"),
                 ("2", "3", "4", "12", "pdl"), ("2", "5", "4", "8", "pdl")]
+    if "--late" in sys.argv:
+        # BP: fewer view chunks from the third phase on (TG_E2E_CHUNKS_LATE)
+        grid = [("2", "3", "4", "8", "pdl"), ("2", "3", "4", "8", "late2"), ("2", "3", "4", "8", "late1"),
+                ("2", "3", "4", "8", "late3"), ("2", "4", "4", "8", "late2"), ("2", "2", "4", "8", "late2"),
+                ("2", "3", "6", "8", "late2"), ("2", "3", "4", "8", "pdl")]
+    if "--late2" in sys.argv:
+        grid = [("2", "3", "4", "8", "late2from1"), ("2", "3", "4", "8", "late2from2"),
+                ("2", "3", "4", "8", "late2from3"), ("2", "4", "4", "8", "late2from1"),
+                ("2", "4", "4", "8", "late1from3"), ("2", "3", "5", "8", "late2from1"),
+                ("1", "3", "4", "8", "late2from1"), ("2", "3", "4", "8", "late2from2")]
     if "--grid1" in sys.argv:
         grid = [("2", "2", "4", "8", "pdl"), ("2", "2", "4", "8", "nopdl")]
     for c, r, ch, g, mode in grid:
@@ -92,6 +102,11 @@ def sweep():
                    TG_E2E_GROUP=g)
         if mode == "nopdl":
             env["TG_E2E_NOPDL"] = "1"
+        if mode.startswith("late"):
+            late, _, frm = mode[4:].partition("from")
+            env["TG_E2E_CHUNKS_LATE"] = late
+            if frm:
+                env["TG_E2E_LATE_FROM"] = frm
         subprocess.run([sys.executable, os.path.abspath(__file__)], env=env, timeout=300)
 
 
