@@ -1839,10 +1839,15 @@ void phased_backproject(tg_cone_plan& p, uint64_t z0, uint64_t nz, uint64_t v0, 
   // schedule cost 40.2 ms serialised against 36.5 for one launch (launch
   // tails).  c4: 40.27 -> 39.42 ms with 2 chunks from phase 2 (1 chunk 45.1,
   // from phase 1 41.5; scripts/e2e_variants.py --late / --late2,
-  // profiles/r2_e2e_late_sweep.jsonl)
-  const int kChunksLate = fdk ? kChunks : knob("TG_E2E_CHUNKS_LATE", 2);
+  // profiles/r2_e2e_late_sweep.jsonl).  The FDK schedule, bound by the copy
+  // engine (whole detector rows), keeps uniform chunks: 45.4 ms against
+  // 46.8-51.9 with fewer late chunks.
+  const int kChunksLate = knob("TG_E2E_CHUNKS_LATE", fdk ? kChunks : 2);
   const int kLateFrom = knob("TG_E2E_LATE_FROM", 2);
-  const uint64_t chunk_late = ((np + kChunksLate - 1) / kChunksLate + kGroup - 1) / kGroup * kGroup;
+  // (FDK: whole early chunks, each its own copy group)
+  const uint64_t chunk_late =
+      fdk ? chunk * uint64_t((n_chunks + kChunksLate - 1) / kChunksLate)
+          : ((np + kChunksLate - 1) / kChunksLate + kGroup - 1) / kGroup * kGroup;
   const int n_chunks_late = int((np + chunk_late - 1) / chunk_late);
   const int n_phases = int(phases.size());
   // consecutive K1 launches overlap (programmatic dependent launch); never a
@@ -1931,10 +1936,14 @@ void phased_backproject(tg_cone_plan& p, uint64_t z0, uint64_t nz, uint64_t v0, 
   };
   // rows [ra, rb) of views [w0, w0 + wn) just uploaded, to be weighted and
   // filtered in place once they land (FDK)
-  std::vector<std::pair<int64_t, int64_t>> fresh;
+  struct Fresh {
+    uint64_t w0, wn;  // views
+    int64_t ra, rb;   // rows
+  };
+  std::vector<Fresh> fresh;
   auto upload = [&](uint64_t w0, uint64_t wn, int64_t ua, int64_t ub, int64_t ra, int64_t rb) {
     if (ub <= ua || rb <= ra || wn == 0) return;
-    if (fdk) fresh.push_back({ra, rb});
+    if (fdk) fresh.push_back({w0, wn, ra, rb});
     cudaMemcpy3DParms cp = {};
     // host views sit h_view_pitch elements apart (the band itself, or the
     // rows of a full sinogram)
@@ -1985,14 +1994,14 @@ void phased_backproject(tg_cone_plan& p, uint64_t z0, uint64_t nz, uint64_t v0, 
       TG_CUDA(cudaStreamWaitEvent(hp.cs, hp.ev[ev++], 0));
       const bool filtered = !fresh.empty();
       bool first_seg = true;
-      for (const auto& sg : fresh) {  // FDK: cosine x Parker + Ram-Lak on the new rows
+      for (const Fresh& sg : fresh) {  // FDK: cosine x Parker + Ram-Lak on the new rows
         filt::RowLayout lay;
-        lay.rows_per_view = uint64_t(sg.second - sg.first);
+        lay.rows_per_view = uint64_t(sg.rb - sg.ra);
         lay.view_pitch = n_rows * nu;
-        float* seg = d_band + (w0 * n_rows + uint64_t(sg.first) - v0) * nu;
+        float* seg = d_band + (sg.w0 * n_rows + uint64_t(sg.ra) - v0) * nu;
         // the chunk's first pre-weights pass overlaps the previous K1's tail
         // (that K1 reads other views' rows; the pass waits for it before exiting)
-        prefilter_impl(p, seg, seg, use_parker, uint64_t(sg.first), lay.rows_per_view, w0, wn,
+        prefilter_impl(p, seg, seg, use_parker, uint64_t(sg.ra), lay.rows_per_view, sg.w0, sg.wn,
                        hp.cs, lay, kPdl && first_seg && k1_last);
         first_seg = false;
       }

@@ -95,6 +95,12 @@ def sweep():
                 ("2", "3", "4", "8", "late2from3"), ("2", "4", "4", "8", "late2from1"),
                 ("2", "4", "4", "8", "late1from3"), ("2", "3", "5", "8", "late2from1"),
                 ("1", "3", "4", "8", "late2from1"), ("2", "3", "4", "8", "late2from2")]
+    if "--fdklate" in sys.argv:
+        os.environ["E2E_FDK"] = "1"
+        grid = [("1", "5", "3", "8", "pdl"), ("1", "5", "3", "8", "late2from2"),
+                ("1", "5", "3", "8", "late1from2"), ("1", "5", "3", "8", "late1from3"),
+                ("1", "5", "4", "8", "late2from2"), ("1", "5", "4", "8", "late1from2"),
+                ("1", "4", "3", "8", "late1from2"), ("1", "5", "3", "8", "pdl")]
     if "--grid1" in sys.argv:
         grid = [("2", "2", "4", "8", "pdl"), ("2", "2", "4", "8", "nopdl")]
     for c, r, ch, g, mode in grid:
