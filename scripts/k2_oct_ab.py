@@ -1,9 +1,9 @@
-"""[Experiment record: the TG_K2_PLANE variant was removed after this
+"""[Experiment record: the TG_K2_OCT variant was removed after this
 measurement, profiles/r2_k2_bank_model.txt.]
-K2 quad kernel with plane quads (TG_K2_PLANE=1: 2x2 transverse quads per
-plane of the ray's dominant axis, one gather per dominant-cell step) against
-the plain quad kernel, forced k2_impl 0, at c4 (all 496 views) and c5 (views
-0-89), with a bitwise comparison; the slab kernel's time on the same views."""
+K2 quad kernel with the OCT layout (TG_K2_OCT=1: one 32-byte cell of the
+8 taps per trilinear cell, one 256-bit gather per sample, FP32x2 lerps)
+against the plain quad kernel, forced k2_impl 0, at c4 (all 496 views) and c5
+(views 0-89), with a bitwise comparison; the slab kernel on the same views."""
 import json
 import math
 import os
@@ -32,7 +32,7 @@ def run(cfg):
     res = {"cfg": cfg}
     ref = None
     for mix in ("0", "1", "0", "1"):
-        os.environ["TG_K2_PLANE"] = mix
+        os.environ["TG_K2_OCT"] = mix
         tg.cone_forward_views(geo, ph, v0, nv, out=out)
         torch.cuda.synchronize()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -40,11 +40,11 @@ def run(cfg):
         tg.cone_forward_views(geo, ph, v0, nv, out=out)
         b.record()
         torch.cuda.synchronize()
-        res.setdefault(f"plane{mix}_ms", []).append(a.elapsed_time(b))
+        res.setdefault(f"oct{mix}_ms", []).append(a.elapsed_time(b))
         if ref is None:
             ref = out.clone()
         else:
-            res[f"plane{mix}_bitwise"] = bool(torch.equal(out, ref))
+            res[f"oct{mix}_bitwise"] = bool(torch.equal(out, ref))
     tg.set_cone_knob(geo, "k2_impl", 1)
     tg.cone_forward_views(geo, ph, v0, nv, out=out)
     torch.cuda.synchronize()
