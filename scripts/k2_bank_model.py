@@ -73,8 +73,8 @@ def schedule(cell, N, hh, dax, T):
         kk = np.minimum(kk + 2 * pairs, N)
     return its, d0s
 
-def sim(cfg, view, u0, v0, layouts, warp=(8, 4), T=8):
-    TU = TV = 16
+def sim(cfg, view, u0, v0, layouts, warp=(8, 4), T=8, tile=(16, 16)):
+    TU, TV = tile
     o, e, t0, dt, ns, hit = rays(cfg, view, u0, v0, TU, TV)
     if hit.sum() == 0: return None
     es = e[hit].sum(0)
@@ -110,13 +110,17 @@ def sim(cfg, view, u0, v0, layouts, warp=(8, 4), T=8):
 if __name__ == '__main__':
     cfg = sys.argv[1]
     warp = tuple(int(x) for x in sys.argv[2].split('x')) if len(sys.argv) > 2 else (8, 4)
+    tile = tuple(int(x) for x in sys.argv[3].split('x')) if len(sys.argv) > 3 else (16, 16)
+    ncase = int(sys.argv[4]) if len(sys.argv) > 4 else 60
     rs = np.random.RandomState(1)
     n, sp, nu, nv, du, nviews, rng = geom(cfg)
-    cases = [(int(rs.randint(nviews)), int(rs.randint(nu // 16)) * 16, int(rs.randint(nv // 16)) * 16) for _ in range(60)]
-    layouts = [(40, 24), (40, 22), (40, 21), (40, 23), (44, 24), (36, 24), (48, 24), (52, 24), (56, 24), (72, 24), (68, 24), (32, 24)]
+    cases = [(int(rs.randint(nviews)), int(rs.randint(nu // tile[0])) * tile[0],
+              int(rs.randint(nv // tile[1])) * tile[1]) for _ in range(ncase)]
+    layouts = [(40, 24), (44, 24), (36, 24), (48, 24), (52, 24), (56, 24), (72, 24), (68, 24),
+               (32, 24), (40, 12), (44, 12), (48, 12), (52, 12), (36, 12)]
     tot = {L: [0, 0] for L in layouts}
     for v, u0, v0 in cases:
-        r = sim(cfg, v, u0, v0, layouts, warp)
+        r = sim(cfg, v, u0, v0, layouts, warp, tile=tile)
         if r:
             for L in layouts: tot[L][0] += r[L][0]; tot[L][1] += r[L][1]
     for L in layouts:
