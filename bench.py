@@ -265,6 +265,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-fdk-e2e", action="store_true",
                     help="skip the FDK-from-host-sinogram leg (tg_cone_fdk_host)")
+    ap.add_argument("--no-calibrated", action="store_true",
+                    help="skip the calibrated-matrix (general K1 path) leg")
     ap.add_argument("--fp-steps", type=int, default=3)
     ap.add_argument("--c5-iters", type=int, default=2,
                     help="TV-loop iterations timed at config c5 (0 = skip the c5 leg)")
@@ -477,6 +479,39 @@ def main():
                    "max_rel_diff_vs_device": fdk_parity}
         del h_sino, h_vol
 
+    # ---- K1 with calibrated (non-circular) matrices: the general path ----------
+    # (scanners with measured projection matrices).  The c4
+    # matrices with a small detector tilt / skew and out-of-plane terms,
+    # normalised by set_matrices; device-resident full detector, CUDA events.
+    k1_cal = None
+    if world == 1 and not args.no_calibrated:
+        import numpy as np
+        m = np.asarray(geo.matrices).reshape(-1, 12).copy()
+        rng = np.random.default_rng(11)
+        m[:, [0, 1, 4, 5]] *= 1.0 + 2e-4 * rng.standard_normal((m.shape[0], 4))
+        m[:, 2] += 2e-3 * rng.standard_normal(m.shape[0])   # P[0][2] != 0
+        m[:, 10] += 1e-5 * rng.standard_normal(m.shape[0])  # P[2][2] != 0
+        cgeo = tg.make_cone_from_matrices(geo.volume, geo.detector, geo.angular_range, geo.sid,
+                                          geo.sdd, m)
+        csino = bump_band(torch, C4["views"], 0, C4["nv"], C4["nu"], dev)
+        cvol = torch.empty((C4["n"],) * 3, dtype=torch.float32, device=dev)
+        for _ in range(2):
+            tg.cone_backproject_slab(cgeo, csino, 0, C4["n"], 0, out=cvol)
+        torch.cuda.synchronize()
+        ca, cb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        n_cal = 4
+        ca.record()
+        for _ in range(n_cal):
+            tg.cone_backproject_slab(cgeo, csino, 0, C4["n"], 0, out=cvol)
+        cb.record()
+        torch.cuda.synchronize()
+        cal_ms = ca.elapsed_time(cb) / n_cal
+        k1_cal = {"value": C4["n"] ** 3 * C4["views"] / (cal_ms / 1e3) / 1e9, "unit": UNIT,
+                  "ms": cal_ms, "circular": bool(cgeo.circular),
+                  "workload": "c4 volume / detector / views with perturbed (calibrated) projection "
+                              "matrices: general per-voxel K1 path"}
+        del csino, cvol, cgeo
+
     # ---- roofline (K1) --------------------------------------------------------
     pk = peaks()
     sm_max = float(pk.get("sm_max_mhz", 1965.0))
@@ -567,6 +602,7 @@ def main():
                    "measured_gather_ceiling_gsamples": 611.0,
                    "measured_gather_ceiling_frac": fp_value / 611.0},
             "fdk_e2e": fdk_e2e,
+            "k1_calibrated": k1_cal,
             "k3_fdk_prefilter_ms": k3_ms, "k1_ms_mean": k1_avg, "k1_ms_min": min(k1_ms),
             # FDK of this rank's slab (pipelines.hpp:73-84): K3 on the band + K1
             "fdk_ms": k3_ms + k1_avg,
