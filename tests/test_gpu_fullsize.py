@@ -102,3 +102,23 @@ def test_c4_linearity_determinism_slabs(tg, c4):
         v0, nr = tg.cone_slab_rows(c4, z0, nz)
         slab = tg.cone_backproject_slab(c4, p[:, v0:v0 + nr].contiguous(), z0, nz, v0)
         assert torch.equal(slab, a[z0:z0 + nz])
+
+
+def test_c4_calibrated_slices_vs_oracle(tg, O, c4):
+    """the general (non-circular) K1 path at full c4 size: perturbed projection
+    matrices (detector tilt / skew, out-of-plane terms; bench.py's
+    k1_calibrated leg) through set_matrices, 12 z-slices in 3 groups against
+    the oracle's back-projection with the same matrices"""
+    m = np.asarray(c4.matrices).reshape(-1, 12).copy()
+    rng = np.random.default_rng(11)
+    m[:, [0, 1, 4, 5]] *= 1.0 + 2e-4 * rng.standard_normal((m.shape[0], 4))
+    m[:, 2] += 2e-3 * rng.standard_normal(m.shape[0])
+    m[:, 10] += 1e-5 * rng.standard_normal(m.shape[0])
+    geo = tg.make_cone_from_matrices(c4.volume, c4.detector, c4.angular_range, c4.sid, c4.sdd, m)
+    assert not geo.circular
+    raw = _bump(0.7)
+    vol = tg.back_project(tg.Sinogram.cone_beam(496, geo.detector, data=raw), geo).data
+    r_np = raw.cpu().numpy()
+    for z0 in (0, 254, 508):
+        ref = O.cone_backproject(_oracle_slab(O, geo, z0, 4), r_np)
+        assert_close(vol[z0:z0 + 4].cpu().numpy(), ref, what=f"c4 calibrated BP slices {z0}")
