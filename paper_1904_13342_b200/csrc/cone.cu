@@ -716,6 +716,7 @@ __global__ void __launch_bounds__(256, TU == 32 ? 5 : 4) cone_fp_kernel(const Fp
     const double cx = floor(ax), cy = floor(ay), cz = floor(az);
     const float bx = float(ax - cx), by = float(ay - cy), bz = float(az - cz);
     const float4* cell = vbase + (long long)cz * nxyp + (long long)cy * sy + (long long)cx * sx;
+    const float4* cell1 = cell + nxyp;  // the same cell one slice up
     const int m = int(min(64LL, n - k0));
     float sum = 0.0f;
     // samples advance by at most half a voxel, so consecutive samples often
@@ -734,8 +735,14 @@ __global__ void __launch_bounds__(256, TU == 32 ? 5 : 4) cone_fp_kernel(const Fp
       const int off = (__float_as_int(tx) - MAGIC_BITS) * sx + (__float_as_int(ty) - MAGIC_BITS) * sy +
                       (__float_as_int(tz) - MAGIC_BITS) * nxyp;
       if (off != prev) {
-        q0 = __ldg(cell + off);         // slice z:   x/x+1 at y, y+1
-        q1 = __ldg(cell + off + nxyp);  // slice z+1
+        // one IMAD.WIDE per address (a signed 32-bit offset scaled into the
+        // 64-bit base) instead of the sign-extend / shift / add chain
+        const float4* c0 = reinterpret_cast<const float4*>(
+            reinterpret_cast<const char*>(cell) + (long long)off * 16);
+        const float4* c1 = reinterpret_cast<const float4*>(
+            reinterpret_cast<const char*>(cell1) + (long long)off * 16);
+        q0 = __ldg(c0);  // slice z:   x/x+1 at y, y+1
+        q1 = __ldg(c1);  // slice z+1
         prev = off;
       }
       const float c0 = lerpf(lerpf(q0.x, q0.y, wx), lerpf(q0.z, q0.w, wx), wy);
