@@ -589,8 +589,9 @@ struct FpArgs {
   double step;                    // march_step: 0.5 * min pitch
   const double* __restrict__ geo;  // per view: source (3) + inverse block (9)
   // zero-bordered "quad" volume, +2 on each side: element (x, y, z) holds
-  // (V[z][y][x], V[z][y][x+1], V[z][y+1][x], V[z][y+1][x+1]), so one
-  // trilinear sample is two 16-byte gathers (slices z and z+1)
+  // (V[z][y][x], V[z][y+1][x], V[z][y][x+1], V[z][y+1][x+1]), so one
+  // trilinear sample is two 16-byte gathers (slices z and z+1) and the two
+  // x-lerps of a slice are one FP32x2 pair
   const float4* __restrict__ vq;
   // the same quads in y-fastest order (index y + x * nyp + z * nxp * nyp):
   // views whose rays run mostly along x gather from it, so the 8 u-lanes of
@@ -745,8 +746,15 @@ __global__ void __launch_bounds__(256, TU == 32 ? 5 : 4) cone_fp_kernel(const Fp
         q1 = __ldg(c1);  // slice z+1
         prev = off;
       }
-      const float c0 = lerpf(lerpf(q0.x, q0.y, wx), lerpf(q0.z, q0.w, wx), wy);
-      const float c1 = lerpf(lerpf(q1.x, q1.y, wx), lerpf(q1.z, q1.w, wx), wy);
+      // quads hold (x, y), (x, y+1), (x+1, y), (x+1, y+1): both x-lerps of a
+      // slice as one FP32x2 pair (the scalar kernel's per-lane operations)
+      const float2 wx2 = make_float2(wx, wx);
+      const float2 t0 = __ffma2_rn(wx2, __fadd2_rn(make_float2(q0.z, q0.w), make_float2(-q0.x, -q0.y)),
+                                   make_float2(q0.x, q0.y));
+      const float2 t1 = __ffma2_rn(wx2, __fadd2_rn(make_float2(q1.z, q1.w), make_float2(-q1.x, -q1.y)),
+                                   make_float2(q1.x, q1.y));
+      const float c0 = lerpf(t0.x, t0.y, wy);
+      const float c1 = lerpf(t1.x, t1.y, wy);
       sum += lerpf(c0, c1, wz);
     }
     total += double(sum);
@@ -793,7 +801,7 @@ __global__ void pad_volume_kernel(const float* __restrict__ vol, float4* __restr
         if (x1) q.w = __ldg(s + (long long)(y + 1) * nx + x + 1);
       }
     }
-    vq[i] = q;
+    vq[i] = make_float4(q.x, q.z, q.y, q.w);  // (x, y), (x, y+1), (x+1, y), (x+1, y+1)
   }
 }
 
@@ -821,7 +829,7 @@ __global__ void pad_volume_t_kernel(const float* __restrict__ vol, float4* __res
         if (x1) q.w = __ldg(s + (long long)(y + 1) * nx + x + 1);
       }
     }
-    vqt[i] = q;
+    vqt[i] = make_float4(q.x, q.z, q.y, q.w);
   }
 }
 
