@@ -707,6 +707,8 @@ __global__ void __launch_bounds__(256, TU == 32 ? 5 : 4) cone_fp_kernel(const Fp
   const int sx = xdom ? a.nyp : 1, sy = xdom ? 1 : a.nxp;
   constexpr float MAGIC = 12582912.0f;  // 1.5 * 2^23: t = M + floor(p) under round-down
   constexpr int MAGIC_BITS = 0x4B400000;
+  const uint32_t usx = uint32_t(sx), usy = uint32_t(sy), unxyp = uint32_t(nxyp);
+  const uint32_t mbias = uint32_t(MAGIC_BITS) * (usx + usy + unxyp);
   double total = 0.0;
   for (long long k0 = 0; k0 < n; k0 += 64) {
     // chunk anchor split into an integer cell and a small fp32 offset, so
@@ -733,8 +735,10 @@ __global__ void __launch_bounds__(256, TU == 32 ? 5 : 4) cone_fp_kernel(const Fp
       const float pz = fmaf(float(j), fdz, bz);
       const float tx = __fadd_rd(px, MAGIC), ty = __fadd_rd(py, MAGIC), tz = __fadd_rd(pz, MAGIC);
       const float wx = px - (tx - MAGIC), wy = py - (ty - MAGIC), wz = pz - (tz - MAGIC);
-      const int off = (__float_as_int(tx) - MAGIC_BITS) * sx + (__float_as_int(ty) - MAGIC_BITS) * sy +
-                      (__float_as_int(tz) - MAGIC_BITS) * nxyp;
+      // the three magic biases folded into one constant: exact in 32-bit
+      // modular arithmetic, since the true offset fits in an int
+      const int off = int(__float_as_uint(tx) * usx + __float_as_uint(ty) * usy +
+                          __float_as_uint(tz) * unxyp - mbias);
       if (off != prev) {
         // one IMAD.WIDE per address (a signed 32-bit offset scaled into the
         // 64-bit base) instead of the sign-extend / shift / add chain
