@@ -598,6 +598,8 @@ struct FpArgs {
   // a warp (which then step along y) read neighbouring quads
   const float4* __restrict__ vqT;
   int nxp, nyp;                   // padded extents (x, y)
+  // MAGIC_BITS * (sx + sy + nxp * nyp) mod 2^32 for the x- / y-fastest quads
+  uint32_t mbias, mbias_t;
   float* out;                     // [n_views][nv][nu]
 };
 
@@ -706,9 +708,9 @@ __global__ void __launch_bounds__(256, TU == 32 ? 5 : 4) cone_fp_kernel(const Fp
   const float4* vbase = xdom ? a.vqT : a.vq;
   const int sx = xdom ? a.nyp : 1, sy = xdom ? 1 : a.nxp;
   constexpr float MAGIC = 12582912.0f;  // 1.5 * 2^23: t = M + floor(p) under round-down
-  constexpr int MAGIC_BITS = 0x4B400000;
   const uint32_t usx = uint32_t(sx), usy = uint32_t(sy), unxyp = uint32_t(nxyp);
-  const uint32_t mbias = uint32_t(MAGIC_BITS) * (usx + usy + unxyp);
+  // (sx + sy = nxp + 1 or nyp + 1: the bias is a launch constant per layout)
+  const uint32_t mbias = xdom ? a.mbias_t : a.mbias;
   double total = 0.0;
   for (long long k0 = 0; k0 < n; k0 += 64) {
     // chunk anchor split into an integer cell and a small fp32 offset, so
@@ -728,11 +730,12 @@ __global__ void __launch_bounds__(256, TU == 32 ? 5 : 4) cone_fp_kernel(const Fp
     // wavefronts; K2 is bound by the L1 data pipe)
     int prev = 0x7fffffff;
     float4 q0 = make_float4(0.f, 0.f, 0.f, 0.f), q1 = q0;
+    float jf = 0.0f;  // float(j), exact (j < 64)
 #pragma unroll 2
-    for (int j = 0; j < m; ++j) {
-      const float px = fmaf(float(j), fdx, bx);
-      const float py = fmaf(float(j), fdy, by);
-      const float pz = fmaf(float(j), fdz, bz);
+    for (int j = 0; j < m; ++j, jf += 1.0f) {
+      const float px = fmaf(jf, fdx, bx);
+      const float py = fmaf(jf, fdy, by);
+      const float pz = fmaf(jf, fdz, bz);
       const float tx = __fadd_rd(px, MAGIC), ty = __fadd_rd(py, MAGIC), tz = __fadd_rd(pz, MAGIC);
       const float wx = px - (tx - MAGIC), wy = py - (ty - MAGIC), wz = pz - (tz - MAGIC);
       // the three magic biases folded into one constant: exact in 32-bit
@@ -748,8 +751,8 @@ __global__ void __launch_bounds__(256, TU == 32 ? 5 : 4) cone_fp_kernel(const Fp
             reinterpret_cast<const char*>(cell1) + (long long)off * 16);
         q0 = __ldg(c0);  // slice z:   x/x+1 at y, y+1
         q1 = __ldg(c1);  // slice z+1
-        prev = off;
       }
+      prev = off;  // (unconditional: a register rename, no move)
       // quads hold (x, y), (x, y+1), (x+1, y), (x+1, y+1): both x-lerps of a
       // slice as one FP32x2 pair (the scalar kernel's per-lane operations)
       const float2 wx2 = make_float2(wx, wx);
@@ -1218,6 +1221,9 @@ FpArgs fp_args(const tg_cone_plan& p) {
   a.vqT = p.k2_dual ? p.d_vpad + p.vpad_elems / 2 : nullptr;
   a.nxp = nx + 4;
   a.nyp = ny + 4;
+  const uint32_t nxyp = uint32_t(a.nxp) * uint32_t(a.nyp);
+  a.mbias = 0x4B400000u * (1u + uint32_t(a.nxp) + nxyp);
+  a.mbias_t = 0x4B400000u * (uint32_t(a.nyp) + 1u + nxyp);
   return a;
 }
 
