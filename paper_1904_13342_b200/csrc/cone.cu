@@ -731,13 +731,19 @@ __global__ void __launch_bounds__(256, TU == 32 ? 5 : 4) cone_fp_kernel(const Fp
     int prev = 0x7fffffff;
     float4 q0 = make_float4(0.f, 0.f, 0.f, 0.f), q1 = q0;
     float jf = 0.0f;  // float(j), exact (j < 64)
+    // x and y of the sample position, floor and fraction as FP32x2 pairs
+    // (per lane the scalar FFMA / FADD of the reference order)
+    const float2 fdxy = make_float2(fdx, fdy), bxy = make_float2(bx, by);
+    const float2 M2 = make_float2(MAGIC, MAGIC), nM2 = make_float2(-MAGIC, -MAGIC);
 #pragma unroll 2
     for (int j = 0; j < m; ++j, jf += 1.0f) {
-      const float px = fmaf(jf, fdx, bx);
-      const float py = fmaf(jf, fdy, by);
+      const float2 pxy = __ffma2_rn(make_float2(jf, jf), fdxy, bxy);
       const float pz = fmaf(jf, fdz, bz);
-      const float tx = __fadd_rd(px, MAGIC), ty = __fadd_rd(py, MAGIC), tz = __fadd_rd(pz, MAGIC);
-      const float wx = px - (tx - MAGIC), wy = py - (ty - MAGIC), wz = pz - (tz - MAGIC);
+      const float2 txy = __fadd2_rd(pxy, M2);
+      const float tz = __fadd_rd(pz, MAGIC);
+      const float2 fxy = __fadd2_rn(txy, nM2);
+      const float2 wxy = __fadd2_rn(pxy, make_float2(-fxy.x, -fxy.y));
+      const float tx = txy.x, ty = txy.y, wx = wxy.x, wy = wxy.y, wz = pz - (tz - MAGIC);
       // the three magic biases folded into one constant: exact in 32-bit
       // modular arithmetic, since the true offset fits in an int
       const int off = int(__float_as_uint(tx) * usx + __float_as_uint(ty) * usy +
