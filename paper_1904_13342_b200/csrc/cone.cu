@@ -672,13 +672,14 @@ __device__ __forceinline__ float lerpf(float a, float b, float w) { return fmaf(
 // of streaming the whole volume from HBM once per view.
 // Each warp covers 8 u x 4 v pixels (its rays stay close together in 3D:
 // fewer cache lines per gather than a 32-wide row of pixels).
-// Occupancy: 5 CTAs/SM (48 registers; the few spills sit in the FP64 ray
-// setup) for the 8-row-band variant used while the volume's slices are small
-// (c4: 442.7 -> 432.7 ms, bitwise-identical output), 4 CTAs/SM (64 registers)
+// Occupancy: 6 CTAs/SM (40 registers; the spills sit in the FP64 ray setup)
+// for the 8-row-band variant used while the volume's slices are small (c4:
+// 442.7 -> 432.7 ms at 5 CTAs; 401.5 -> 399.2 ms at 6 once the march loop
+// was trimmed to ~27 instructions per sample), 4 CTAs/SM (64 registers)
 // for the 4-row-band variant of large volumes (c5: 5 CTAs measured 0.7% slower,
 // 6 CTAs 6.5%; profiles/r1_k2_occupancy.txt).
 template <int TU>
-__global__ void __launch_bounds__(256, TU == 32 ? 5 : 4) cone_fp_kernel(const FpArgs a) {
+__global__ void __launch_bounds__(256, TU == 32 ? 6 : 4) cone_fp_kernel(const FpArgs a) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   constexpr int WPR = TU / 8;  // 8 u x 4 v warps, TU / 8 of them per 4-row band
   const int iu = blockIdx.x * TU + (w % WPR) * 8 + (lane & 7);
