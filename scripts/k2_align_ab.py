@@ -1,4 +1,6 @@
-"""K2 quad kernel: plane-aligned lane schedule (TG_K2_ALIGN=1: 5 CTAs/SM,
+"""[Experiment record: the TG_K2_ALIGN variant was removed after this
+measurement, profiles/r2_k2_align_ab.txt.]
+K2 quad kernel: plane-aligned lane schedule (TG_K2_ALIGN=1: 5 CTAs/SM,
 2: 4 CTAs/SM, 3: 6 CTAs/SM) against the lock-step kernel (TG_K2_ALIGN=0),
 forced k2_impl 0 (quad volume), at c4 (all 496 views) and c5 (views 0-89),
 with a bitwise comparison against the lock-step output."""

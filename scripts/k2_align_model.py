@@ -1,3 +1,7 @@
+"""Offline model for profiles/r2_k2_align_ab.txt: distinct 128-byte lines per
+K2 quad gather instruction (8u x 4v warps, c4 geometry, cell reuse) for the
+lock-step and the plane-aligned lane schedules.  Usage: python k2_align_model.py
+[view angle in rad]."""
 import numpy as np, sys
 rng=np.random.default_rng(0)
 N=512; sp=0.5; org=-(N-1)/2*sp  # centered voxel centres
@@ -54,7 +58,7 @@ def warp_cost(theta, u0, v0, align):
         if ld.any():
             lines+=len(np.unique((off[ld]*16)//128)); loads+=ld.sum()
     return lines,samples,loads,iters
-import math
+theta=float(sys.argv[1]) if len(sys.argv)>1 else 0.5
 tot={False:[0,0,0,0],True:[0,0,0,0]}
 for w in range(300):
     u0=8*rng.integers(0,nu//8); v0=4*rng.integers(0,nv//4)
