@@ -24,7 +24,7 @@ def main():
     modes = sys.argv[1:] or ["0", "1", "2", "3", "4"]
     ref = None
     for m in modes:
-        os.environ["TG_K3_X2"] = m
+        os.environ[os.environ.get("KNOB", "TG_K3_X2")] = m
         band = tg.fdk_prefilter(raw, geo, True, v0=me.v0)
         torch.cuda.synchronize()
         ts = []
