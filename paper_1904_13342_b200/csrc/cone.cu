@@ -688,10 +688,10 @@ __global__ void __launch_bounds__(256, TU == 32 ? 6 : 4) cone_fp_kernel(const Fp
   if (iu >= a.nu || iv >= a.nv) return;
   double o[3], d[3], t0, t1;
   float* out = a.out + ((long long)vl * a.nv + iv) * a.nu + iu;
-  if (!cone_ray(a, iu, iv, a.view0 + vl, o, d, t0, t1)) {
-    *out = 0.0f;
-    return;
-  }
+  // a missed ray's zero is stored with its warp's other results (one store
+  // instruction per warp)
+  const bool hit = cone_ray(a, iu, iv, a.view0 + vl, o, d, t0, t1);
+  auto march = [&]() -> float {
   const double span = DADD(t1, -t0);
   const long long n = ray_sample_count(span, a.step);
   const double dt = DDIV(span, double(n));
@@ -773,7 +773,10 @@ __global__ void __launch_bounds__(256, TU == 32 ? 6 : 4) cone_fp_kernel(const Fp
     }
     total += double(sum);
   }
-  *out = float(total * dt);
+  return float(total * dt);
+  };
+  const float res = hit ? march() : 0.0f;
+  *out = res;
 }
 
 // Diagnostic: the per-ray sample count K2 marches (0 = missed ray), same

@@ -325,8 +325,7 @@ __global__ void __launch_bounds__(NTHREADS, 2)
       out = f.out + ((long long)blockIdx.y * f.nv + iv) * f.nu + iu;
       double o[3], d[3], t0, t1;
       if (!cone_ray(f, iu, iv, view, o, d, t0, t1)) {
-        *out = 0.0f;
-        out = nullptr;
+        // zero stored at the end with the warp's other results (whole sectors)
       } else {
         const double span = DADD(t1, -t0);
         r.n = int(ray_sample_count(span, f.step));
@@ -488,7 +487,7 @@ __global__ void __launch_bounds__(NTHREADS, 2)
   }
   if (out) {
     r.total += double(r.sum);
-    *out = float(r.total * RayRef{rstate->v + tid}.dt());
+    *out = r.n > 0 ? float(r.total * RayRef{rstate->v + tid}.dt()) : 0.0f;
   }
 }
 
