@@ -254,10 +254,11 @@ struct StageHdr {
 // spills sit in the per-view prologue and the partial-tile path, not in the
 // fast loop) and a 6-stage ring (<= 72 KB of boxes per CTA).  Against 2 CTAs
 // at 96 registers: 45.2 -> 41.9 ms at c4.  The general (calibrated) variant
-// keeps 96 registers / 2 CTAs: its per-voxel projective map spills too much
-// at 72 (891 vs 1043 GUPS).
+// too since round 2's FFMA2 loop (no spills in its fast loop at 72): c4
+// calibrated 55.73 -> 53.35 ms against 2 CTAs at 96 registers (80: 55.79;
+// round 1's scalar loop spilled at 72, 891 vs 1043 GUPS).
 template <int K, int BOXU, bool CIRC>
-__global__ void __maxnreg__(CIRC ? 72 : 96)
+__global__ void __maxnreg__(72)
     cone_bp_kernel(const __grid_constant__ CUtensorMap tmap, const BpArgs a) {
   extern __shared__ __align__(128) unsigned char smem[];
   const int box_elems = BOXU * a.boxV;
