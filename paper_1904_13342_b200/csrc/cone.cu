@@ -688,13 +688,15 @@ __global__ void __launch_bounds__(256, TU == 32 ? 6 : 4) cone_fp_kernel(const Fp
   const int vl = blockIdx.y;
   if (iu >= a.nu || iv >= a.nv) return;
   double o[3], d[3], t0, t1;
-  float* out = a.out + ((long long)vl * a.nv + iv) * a.nu + iu;
   // a missed ray's zero is stored with its warp's other results (one store
-  // instruction per warp)
+  // instruction per warp).  Register budget (40 at 6 CTAs/SM): only the FP64
+  // anchor state, the running total and the layout bit live across chunks;
+  // the layout, the fp32 steps, the output address are re-derived where used
+  // (fewer spill reloads at each chunk anchor, profiles/r2_k2_traffic.txt).
   const bool hit = cone_ray(a, iu, iv, a.view0 + vl, o, d, t0, t1);
   auto march = [&]() -> float {
   const double span = DADD(t1, -t0);
-  const long long n = ray_sample_count(span, a.step);
+  const int n = int(ray_sample_count(span, a.step));  // < 2^31 samples per ray
   const double dt = DDIV(span, double(n));
 
   // Sample k sits at t0 + (k + 1/2) dt; march in index space (fp32) from
@@ -704,17 +706,17 @@ __global__ void __launch_bounds__(256, TU == 32 ? 6 : 4) cone_fp_kernel(const Fp
   const double p0y = (o[1] + th * d[1] - a.oy) / a.sy + 2.0;
   const double p0z = (o[2] + th * d[2] - a.oz) / a.sz + 2.0;
   const double ddx = dt * d[0] / a.sx, ddy = dt * d[1] / a.sy, ddz = dt * d[2] / a.sz;
-  const float fdx = float(ddx), fdy = float(ddy), fdz = float(ddz);
-  const int nxyp = a.nxp * a.nyp;
   const bool xdom = a.vqT != nullptr && fabs(d[0]) > fabs(d[1]);
-  const float4* vbase = xdom ? a.vqT : a.vq;
-  const int sx = xdom ? a.nyp : 1, sy = xdom ? 1 : a.nxp;
   constexpr float MAGIC = 12582912.0f;  // 1.5 * 2^23: t = M + floor(p) under round-down
-  const uint32_t usx = uint32_t(sx), usy = uint32_t(sy), unxyp = uint32_t(nxyp);
-  // (sx + sy = nxp + 1 or nyp + 1: the bias is a launch constant per layout)
-  const uint32_t mbias = xdom ? a.mbias_t : a.mbias;
   double total = 0.0;
-  for (long long k0 = 0; k0 < n; k0 += 64) {
+  for (int k0 = 0; k0 < n; k0 += 64) {
+    const int nxyp = a.nxp * a.nyp;
+    const float4* vbase = xdom ? a.vqT : a.vq;
+    const int sx = xdom ? a.nyp : 1, sy = xdom ? 1 : a.nxp;
+    const uint32_t usx = uint32_t(sx), usy = uint32_t(sy), unxyp = uint32_t(nxyp);
+    // (sx + sy = nxp + 1 or nyp + 1: the bias is a launch constant per layout)
+    const uint32_t mbias = xdom ? a.mbias_t : a.mbias;
+    const float fdx = float(ddx), fdy = float(ddy), fdz = float(ddz);
     // chunk anchor split into an integer cell and a small fp32 offset, so
     // sample positions keep ~1e-5 voxel precision anywhere in a 1024^3 grid;
     // per-sample offsets from the cell fit in 32 bits
@@ -723,8 +725,7 @@ __global__ void __launch_bounds__(256, TU == 32 ? 6 : 4) cone_fp_kernel(const Fp
     const double cx = floor(ax), cy = floor(ay), cz = floor(az);
     const float bx = float(ax - cx), by = float(ay - cy), bz = float(az - cz);
     const float4* cell = vbase + (long long)cz * nxyp + (long long)cy * sy + (long long)cx * sx;
-    const float4* cell1 = cell + nxyp;  // the same cell one slice up
-    const int m = int(min(64LL, n - k0));
+    const int m = min(64, n - k0);
     float sum = 0.0f;
     // samples advance by at most half a voxel, so consecutive samples often
     // stay in the same trilinear cell: re-gather only when the cell changes
@@ -752,13 +753,12 @@ __global__ void __launch_bounds__(256, TU == 32 ? 6 : 4) cone_fp_kernel(const Fp
                           __float_as_uint(tz) * unxyp - mbias);
       if (off != prev) {
         // one IMAD.WIDE per address (a signed 32-bit offset scaled into the
-        // 64-bit base) instead of the sign-extend / shift / add chain
+        // 64-bit base) instead of the sign-extend / shift / add chain; the
+        // slice z+1 quad one padded slice further
         const float4* c0 = reinterpret_cast<const float4*>(
             reinterpret_cast<const char*>(cell) + (long long)off * 16);
-        const float4* c1 = reinterpret_cast<const float4*>(
-            reinterpret_cast<const char*>(cell1) + (long long)off * 16);
-        q0 = __ldg(c0);  // slice z:   x/x+1 at y, y+1
-        q1 = __ldg(c1);  // slice z+1
+        q0 = __ldg(c0);           // slice z:   x/x+1 at y, y+1
+        q1 = __ldg(c0 + nxyp);    // slice z+1
       }
       prev = off;  // (unconditional: a register rename, no move)
       // quads hold (x, y), (x, y+1), (x+1, y), (x+1, y+1): both x-lerps of a
@@ -777,7 +777,7 @@ __global__ void __launch_bounds__(256, TU == 32 ? 6 : 4) cone_fp_kernel(const Fp
   return float(total * dt);
   };
   const float res = hit ? march() : 0.0f;
-  *out = res;
+  a.out[((long long)vl * a.nv + iv) * a.nu + iu] = res;
 }
 
 // Diagnostic: the per-ray sample count K2 marches (0 = missed ray), same
