@@ -460,7 +460,7 @@ def main():
 
         for _ in range(3):  # warm-up (fresh pinned buffers, staging allocation)
             fdk_step()
-        n_fdk = 3
+        n_fdk = 6
         fdk_steps_ms = []
         t0 = time.perf_counter()
         for _ in range(n_fdk):
