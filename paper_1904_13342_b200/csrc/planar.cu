@@ -152,7 +152,7 @@ __global__ void __launch_bounds__(256, TG_PLANAR_FP_MINB) planar_fp_kernel(const
     hit = planar_ray(a, i, j, o, d, t0, t1);
     if (hit) {
       const double span = DADD(t1, -t0);
-      const long long n = ray_sample_count(span, a.step);
+      const int n = int(ray_sample_count(span, a.step));  // < 2^31 samples per ray
       dt = DDIV(span, double(n));
       // sample k at t0 + (k + 1/2) dt (projector.hpp:109-128), in padded
       // index coordinates
@@ -160,20 +160,23 @@ __global__ void __launch_bounds__(256, TG_PLANAR_FP_MINB) planar_fp_kernel(const
       const double p0x = (o[0] + th * d[0] - a.ox) / a.sx + 2.0;
       const double p0y = (o[1] + th * d[1] - a.oy) / a.sy + 2.0;
       const double ddx = dt * d[0] / a.sx, ddy = dt * d[1] / a.sy;
-      const float fdx = float(ddx), fdy = float(ddy);
       // rays running mostly along x: adjacent bins are displaced along y,
       // so gather from the y-fastest quads
       const bool xdom = fabs(d[0]) > fabs(d[1]);
-      const float4* base = xdom ? a.qT : a.q;
-      const int stx = xdom ? a.nyp : 1, sty = xdom ? 1 : a.nxp;
       constexpr float MAGIC = 12582912.0f;  // 1.5 * 2^23: t = M + floor(p) under round-down
       constexpr int MAGIC_BITS = 0x4B400000;
-      for (long long k0 = 64LL * seg; k0 < n; k0 += 64LL * S) {
+      for (int k0 = 64 * seg; k0 < n; k0 += 64 * S) {
+        // layout and fp32 steps re-derived per chunk: only the FP64 anchor
+        // state and the layout bit live across chunks (fewer spills at the
+        // 40-register cap; as in K2, profiles/r2_k2_traffic.txt)
+        const float4* base = xdom ? a.qT : a.q;
+        const int stx = xdom ? a.nyp : 1, sty = xdom ? 1 : a.nxp;
+        const float fdx = float(ddx), fdy = float(ddy);
         const double ax = p0x + double(k0) * ddx, ay = p0y + double(k0) * ddy;
         const double cx = floor(ax), cy = floor(ay);
         const float bx = float(ax - cx), by = float(ay - cy);
         const float4* cell = base + (long long)cy * sty + (long long)cx * stx;
-        const int m = int(min(64LL, n - k0));
+        const int m = min(64, n - k0);
         float sum = 0.0f;
         int prev = 0x7fffffff;
         float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
