@@ -130,11 +130,13 @@ __device__ __forceinline__ float rcp_approx(float x) {
 // marching the 64-sample chunks s, s + S, ... of its ray.  The segments'
 // partial sums are combined in shared memory by a fixed pairwise tree
 // ((s0 + s1) + (s2 + s3) ...), so the result does not depend on scheduling.
-// 6 CTAs (48 warps) per SM: the march is L2-latency bound, and a 40-register
-// cap (spills only in the FP64 ray setup) against 64 registers / 4 CTAs:
-// c2 371 -> 320 us, c1 104 -> 99 us (profiles/r2_planar_fp_variants.txt)
+// 7 CTAs (56 warps) per SM at 32 registers: the march is L2-latency bound
+// (64 registers / 4 CTAs -> 40 / 6: c2 371 -> 320 us, c1 104 -> 99 us,
+// profiles/r2_planar_fp_variants.txt; with only the anchor state live across
+// chunks 6 -> 7 CTAs: c2 312.7 -> 291.1 us, c1 97.1 -> 95.6 us; 8 is the same
+// 32-register build)
 #ifndef TG_PLANAR_FP_MINB
-#define TG_PLANAR_FP_MINB 6
+#define TG_PLANAR_FP_MINB 7
 #endif
 template <bool REUSE>
 __global__ void __launch_bounds__(256, TG_PLANAR_FP_MINB) planar_fp_kernel(const FpArgs a) {
@@ -168,7 +170,7 @@ __global__ void __launch_bounds__(256, TG_PLANAR_FP_MINB) planar_fp_kernel(const
       for (int k0 = 64 * seg; k0 < n; k0 += 64 * S) {
         // layout and fp32 steps re-derived per chunk: only the FP64 anchor
         // state and the layout bit live across chunks (fewer spills at the
-        // 40-register cap; as in K2, profiles/r2_k2_traffic.txt)
+        // register cap; as in K2, profiles/r2_k2_traffic.txt)
         const float4* base = xdom ? a.qT : a.q;
         const int stx = xdom ? a.nyp : 1, sty = xdom ? 1 : a.nxp;
         const float fdx = float(ddx), fdy = float(ddy);
