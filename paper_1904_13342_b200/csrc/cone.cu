@@ -695,86 +695,86 @@ __global__ void __launch_bounds__(256, TU == 32 ? 6 : 4) cone_fp_kernel(const Fp
   // (fewer spill reloads at each chunk anchor, profiles/r2_k2_traffic.txt).
   const bool hit = cone_ray(a, iu, iv, a.view0 + vl, o, d, t0, t1);
   auto march = [&]() -> float {
-  const double span = DADD(t1, -t0);
-  const int n = int(ray_sample_count(span, a.step));  // < 2^31 samples per ray
-  const double dt = DDIV(span, double(n));
+    const double span = DADD(t1, -t0);
+    const int n = int(ray_sample_count(span, a.step));  // < 2^31 samples per ray
+    const double dt = DDIV(span, double(n));
 
-  // Sample k sits at t0 + (k + 1/2) dt; march in index space (fp32) from
-  // anchors recomputed in FP64 every 64 samples.
-  const double th = t0 + 0.5 * dt;
-  const double p0x = (o[0] + th * d[0] - a.ox) / a.sx + 2.0;
-  const double p0y = (o[1] + th * d[1] - a.oy) / a.sy + 2.0;
-  const double p0z = (o[2] + th * d[2] - a.oz) / a.sz + 2.0;
-  const double ddx = dt * d[0] / a.sx, ddy = dt * d[1] / a.sy, ddz = dt * d[2] / a.sz;
-  const bool xdom = a.vqT != nullptr && fabs(d[0]) > fabs(d[1]);
-  constexpr float MAGIC = 12582912.0f;  // 1.5 * 2^23: t = M + floor(p) under round-down
-  double total = 0.0;
-  for (int k0 = 0; k0 < n; k0 += 64) {
-    const int nxyp = a.nxp * a.nyp;
-    const float4* vbase = xdom ? a.vqT : a.vq;
-    const int sx = xdom ? a.nyp : 1, sy = xdom ? 1 : a.nxp;
-    const uint32_t usx = uint32_t(sx), usy = uint32_t(sy), unxyp = uint32_t(nxyp);
-    // (sx + sy = nxp + 1 or nyp + 1: the bias is a launch constant per layout)
-    const uint32_t mbias = xdom ? a.mbias_t : a.mbias;
-    const float fdx = float(ddx), fdy = float(ddy), fdz = float(ddz);
-    // chunk anchor split into an integer cell and a small fp32 offset, so
-    // sample positions keep ~1e-5 voxel precision anywhere in a 1024^3 grid;
-    // per-sample offsets from the cell fit in 32 bits
-    const double ax = p0x + double(k0) * ddx, ay = p0y + double(k0) * ddy,
-                 az = p0z + double(k0) * ddz;
-    const double cx = floor(ax), cy = floor(ay), cz = floor(az);
-    const float bx = float(ax - cx), by = float(ay - cy), bz = float(az - cz);
-    const float4* cell = vbase + (long long)cz * nxyp + (long long)cy * sy + (long long)cx * sx;
-    const int m = min(64, n - k0);
-    float sum = 0.0f;
-    // samples advance by at most half a voxel, so consecutive samples often
-    // stay in the same trilinear cell: re-gather only when the cell changes
-    // (lanes that keep their cell are masked off the load and cost no L1
-    // wavefronts; K2 is bound by the L1 data pipe)
-    int prev = 0x7fffffff;
-    float4 q0 = make_float4(0.f, 0.f, 0.f, 0.f), q1 = q0;
-    float jf = 0.0f;  // float(j), exact (j < 64)
-    // x and y of the sample position, floor and fraction as FP32x2 pairs
-    // (per lane the scalar FFMA / FADD of the reference order)
-    const float2 fdxy = make_float2(fdx, fdy), bxy = make_float2(bx, by);
-    const float2 M2 = make_float2(MAGIC, MAGIC), nM2 = make_float2(-MAGIC, -MAGIC);
-#pragma unroll 2
-    for (int j = 0; j < m; ++j, jf += 1.0f) {
-      const float2 pxy = __ffma2_rn(make_float2(jf, jf), fdxy, bxy);
-      const float pz = fmaf(jf, fdz, bz);
-      const float2 txy = __fadd2_rd(pxy, M2);
-      const float tz = __fadd_rd(pz, MAGIC);
-      const float2 fxy = __fadd2_rn(txy, nM2);
-      const float2 wxy = __fadd2_rn(pxy, make_float2(-fxy.x, -fxy.y));
-      const float tx = txy.x, ty = txy.y, wx = wxy.x, wy = wxy.y, wz = pz - (tz - MAGIC);
-      // the three magic biases folded into one constant: exact in 32-bit
-      // modular arithmetic, since the true offset fits in an int
-      const int off = int(__float_as_uint(tx) * usx + __float_as_uint(ty) * usy +
-                          __float_as_uint(tz) * unxyp - mbias);
-      if (off != prev) {
-        // one IMAD.WIDE per address (a signed 32-bit offset scaled into the
-        // 64-bit base) instead of the sign-extend / shift / add chain; the
-        // slice z+1 quad one padded slice further
-        const float4* c0 = reinterpret_cast<const float4*>(
-            reinterpret_cast<const char*>(cell) + (long long)off * 16);
-        q0 = __ldg(c0);           // slice z:   x/x+1 at y, y+1
-        q1 = __ldg(c0 + nxyp);    // slice z+1
+    // Sample k sits at t0 + (k + 1/2) dt; march in index space (fp32) from
+    // anchors recomputed in FP64 every 64 samples.
+    const double th = t0 + 0.5 * dt;
+    const double p0x = (o[0] + th * d[0] - a.ox) / a.sx + 2.0;
+    const double p0y = (o[1] + th * d[1] - a.oy) / a.sy + 2.0;
+    const double p0z = (o[2] + th * d[2] - a.oz) / a.sz + 2.0;
+    const double ddx = dt * d[0] / a.sx, ddy = dt * d[1] / a.sy, ddz = dt * d[2] / a.sz;
+    const bool xdom = a.vqT != nullptr && fabs(d[0]) > fabs(d[1]);
+    constexpr float MAGIC = 12582912.0f;  // 1.5 * 2^23: t = M + floor(p) under round-down
+    double total = 0.0;
+    for (int k0 = 0; k0 < n; k0 += 64) {
+      const int nxyp = a.nxp * a.nyp;
+      const float4* vbase = xdom ? a.vqT : a.vq;
+      const int sx = xdom ? a.nyp : 1, sy = xdom ? 1 : a.nxp;
+      const uint32_t usx = uint32_t(sx), usy = uint32_t(sy), unxyp = uint32_t(nxyp);
+      // (sx + sy = nxp + 1 or nyp + 1: the bias is a launch constant per layout)
+      const uint32_t mbias = xdom ? a.mbias_t : a.mbias;
+      const float fdx = float(ddx), fdy = float(ddy), fdz = float(ddz);
+      // chunk anchor split into an integer cell and a small fp32 offset, so
+      // sample positions keep ~1e-5 voxel precision anywhere in a 1024^3 grid;
+      // per-sample offsets from the cell fit in 32 bits
+      const double ax = p0x + double(k0) * ddx, ay = p0y + double(k0) * ddy,
+                   az = p0z + double(k0) * ddz;
+      const double cx = floor(ax), cy = floor(ay), cz = floor(az);
+      const float bx = float(ax - cx), by = float(ay - cy), bz = float(az - cz);
+      const float4* cell = vbase + (long long)cz * nxyp + (long long)cy * sy + (long long)cx * sx;
+      const int m = min(64, n - k0);
+      float sum = 0.0f;
+      // samples advance by at most half a voxel, so consecutive samples often
+      // stay in the same trilinear cell: re-gather only when the cell changes
+      // (lanes that keep their cell are masked off the load and cost no L1
+      // wavefronts; K2 is bound by the L1 data pipe)
+      int prev = 0x7fffffff;
+      float4 q0 = make_float4(0.f, 0.f, 0.f, 0.f), q1 = q0;
+      float jf = 0.0f;  // float(j), exact (j < 64)
+      // x and y of the sample position, floor and fraction as FP32x2 pairs
+      // (per lane the scalar FFMA / FADD of the reference order)
+      const float2 fdxy = make_float2(fdx, fdy), bxy = make_float2(bx, by);
+      const float2 M2 = make_float2(MAGIC, MAGIC), nM2 = make_float2(-MAGIC, -MAGIC);
+  #pragma unroll 2
+      for (int j = 0; j < m; ++j, jf += 1.0f) {
+        const float2 pxy = __ffma2_rn(make_float2(jf, jf), fdxy, bxy);
+        const float pz = fmaf(jf, fdz, bz);
+        const float2 txy = __fadd2_rd(pxy, M2);
+        const float tz = __fadd_rd(pz, MAGIC);
+        const float2 fxy = __fadd2_rn(txy, nM2);
+        const float2 wxy = __fadd2_rn(pxy, make_float2(-fxy.x, -fxy.y));
+        const float tx = txy.x, ty = txy.y, wx = wxy.x, wy = wxy.y, wz = pz - (tz - MAGIC);
+        // the three magic biases folded into one constant: exact in 32-bit
+        // modular arithmetic, since the true offset fits in an int
+        const int off = int(__float_as_uint(tx) * usx + __float_as_uint(ty) * usy +
+                            __float_as_uint(tz) * unxyp - mbias);
+        if (off != prev) {
+          // one IMAD.WIDE per address (a signed 32-bit offset scaled into the
+          // 64-bit base) instead of the sign-extend / shift / add chain; the
+          // slice z+1 quad one padded slice further
+          const float4* c0 = reinterpret_cast<const float4*>(
+              reinterpret_cast<const char*>(cell) + (long long)off * 16);
+          q0 = __ldg(c0);           // slice z:   x/x+1 at y, y+1
+          q1 = __ldg(c0 + nxyp);    // slice z+1
+        }
+        prev = off;  // (unconditional: a register rename, no move)
+        // quads hold (x, y), (x, y+1), (x+1, y), (x+1, y+1): both x-lerps of a
+        // slice as one FP32x2 pair (the scalar kernel's per-lane operations)
+        const float2 wx2 = make_float2(wx, wx);
+        const float2 t0 = __ffma2_rn(wx2, __fadd2_rn(make_float2(q0.z, q0.w), make_float2(-q0.x, -q0.y)),
+                                     make_float2(q0.x, q0.y));
+        const float2 t1 = __ffma2_rn(wx2, __fadd2_rn(make_float2(q1.z, q1.w), make_float2(-q1.x, -q1.y)),
+                                     make_float2(q1.x, q1.y));
+        const float c0 = lerpf(t0.x, t0.y, wy);
+        const float c1 = lerpf(t1.x, t1.y, wy);
+        sum += lerpf(c0, c1, wz);
       }
-      prev = off;  // (unconditional: a register rename, no move)
-      // quads hold (x, y), (x, y+1), (x+1, y), (x+1, y+1): both x-lerps of a
-      // slice as one FP32x2 pair (the scalar kernel's per-lane operations)
-      const float2 wx2 = make_float2(wx, wx);
-      const float2 t0 = __ffma2_rn(wx2, __fadd2_rn(make_float2(q0.z, q0.w), make_float2(-q0.x, -q0.y)),
-                                   make_float2(q0.x, q0.y));
-      const float2 t1 = __ffma2_rn(wx2, __fadd2_rn(make_float2(q1.z, q1.w), make_float2(-q1.x, -q1.y)),
-                                   make_float2(q1.x, q1.y));
-      const float c0 = lerpf(t0.x, t0.y, wy);
-      const float c1 = lerpf(t1.x, t1.y, wy);
-      sum += lerpf(c0, c1, wz);
+      total += double(sum);
     }
-    total += double(sum);
-  }
-  return float(total * dt);
+    return float(total * dt);
   };
   const float res = hit ? march() : 0.0f;
   a.out[((long long)vl * a.nv + iv) * a.nu + iu] = res;
